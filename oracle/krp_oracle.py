@@ -1,0 +1,295 @@
+"""fp64 CPU oracle for randomized HOSVD / STHOSVD with Khatri-Rao products.
+
+TEST INFRASTRUCTURE.  Plain, slow, obviously-correct numpy (fp64) versions of
+every step of the hot path, written from PAPER.md (arXiv 2507.23207) and cited
+line by line (``P:n`` = line n of PAPER.md).  It shares no code with the CUDA
+path and must only be used by tests/, __graft_entry__.smoke() and bench.py's
+CPU-baseline / reference legs.
+
+Conventions (DESIGN.md §3 readings):
+* Tensors are numpy arrays indexed ``x[i_1, ..., i_d]`` whose flat storage is
+  first-index-fastest: ``x = flat.reshape(dims, order="F")`` (R1).
+* The mode-n unfolding X_(n) is I_n x prod_{k!=n} I_k with column index
+  sum_{k!=n} i_k J_k, J_k = prod_{m<k, m!=n} I_m.  Then
+  (Omega_d ⊙ ... ⊙ Omega_{n+1} ⊙ Omega_{n-1} ⊙ ... ⊙ Omega_1) has its rows in
+  exactly that column order, which is the pairing under which
+  the MTTKRP of Alg. 7 line 3 is the plain matrix product below.
+* Inputs arrive as fp32 and are upcast to fp64 once.
+* Memory-only chunking: a sum over the columns of X_(n) may be split into
+  consecutive last-mode index ranges (``chunk``); this changes only the fp64
+  rounding order, never the terms.  ``chunk=None`` is the unsplit product.
+
+Parity status of each function is recorded in DESIGN.md §4 ("pins"); every
+function here is pinned by a test in tests/test_oracle_pins.py.
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+__all__ = [
+    "as_tensor",
+    "unfold",
+    "fold",
+    "kron",
+    "khatri_rao",
+    "kr_for_mode",
+    "sketch_mode",
+    "sketch_all_modes",
+    "sketch_mode_rows",
+    "thin_qr",
+    "ttm",
+    "multi_ttm",
+    "leading_left_singular_vectors",
+    "rhosvd",
+    "sthosvd",
+    "reconstruct",
+    "tucker_error",
+    "sketch_flops",
+]
+
+
+# ----------------------------------------------------------------- tensor algebra
+def as_tensor(flat: np.ndarray, dims: Sequence[int]) -> np.ndarray:
+    """fp32/fp64 flat first-index-fastest buffer -> fp64 array x[i_1..i_d]."""
+    return np.asarray(flat, dtype=np.float64).reshape(tuple(int(n) for n in dims), order="F")
+
+
+def unfold(x: np.ndarray, n: int) -> np.ndarray:
+    """Mode-n unfolding X_(n): rows i_n, columns = remaining indices,
+    first remaining index fastest."""
+    return np.moveaxis(x, n, 0).reshape(x.shape[n], -1, order="F")
+
+
+def fold(m: np.ndarray, n: int, dims: Sequence[int]) -> np.ndarray:
+    """Inverse of ``unfold``."""
+    dims = tuple(int(v) for v in dims)
+    rest = dims[:n] + dims[n + 1:]
+    return np.moveaxis(m.reshape((dims[n],) + rest, order="F"), 0, n)
+
+
+def kron(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """Kronecker product, block matrix [a_ij * B]."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    m, n = a.shape
+    p, q = b.shape
+    out = np.empty((m * p, n * q))
+    for i in range(m):
+        for j in range(n):
+            out[i * p:(i + 1) * p, j * q:(j + 1) * q] = a[i, j] * b
+    return out
+
+
+def khatri_rao(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """Khatri-Rao (column-wise Kronecker) product: column r = a_r ⊗ b_r."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    assert a.shape[1] == b.shape[1]
+    return np.stack([np.kron(a[:, r], b[:, r]) for r in range(a.shape[1])], axis=1)
+
+
+def kr_for_mode(omegas: Sequence[np.ndarray], n: int) -> np.ndarray:
+    """Omega_d ⊙ ... ⊙ Omega_{n+1} ⊙ Omega_{n-1} ⊙ ... ⊙ Omega_1 (Alg. 7 line 3).
+
+    Formed explicitly, left to right in the paper's order."""
+    others = [np.asarray(omegas[k], dtype=np.float64) for k in range(len(omegas) - 1, -1, -1) if k != n]
+    w = others[0]
+    for o in others[1:]:
+        w = khatri_rao(w, o)
+    return w
+
+
+# ----------------------------------------------------------------- the sketch (MTTKRP)
+def _slab_ranges(last: int, chunk: Optional[int]):
+    if chunk is None or chunk >= last:
+        return [(0, last)]
+    return [(k, min(last, k + chunk)) for k in range(0, last, chunk)]
+
+
+def sketch_mode(x: np.ndarray, omegas: Sequence[np.ndarray], n: int, chunk: Optional[int] = None) -> np.ndarray:
+    """Y_n = X_(n) (Omega_d ⊙ ... ⊙ Omega_{n+1} ⊙ Omega_{n-1} ⊙ ... ⊙ Omega_1)
+    (Alg. 7 line 3; BASELINE north_star), explicit KR times the unfolding.
+
+    ``x`` is the fp64 tensor x[i_1..i_d]; ``omegas[k]`` is I_k x R (omegas[n] unused).
+    With ``chunk``, the columns of X_(n) are taken in last-mode slabs: for n < d-1
+    the slab products are summed, for n = d-1 each slab fills its own rows."""
+    d = x.ndim
+    R = np.asarray(omegas[(n + 1) % d]).shape[1]
+    last = x.shape[-1]
+    if n == d - 1:
+        w = kr_for_mode(omegas, n)  # does not involve Omega_d
+        y = np.zeros((x.shape[n], R))
+        for k0, k1 in _slab_ranges(last, chunk):
+            y[k0:k1] = unfold(x[..., k0:k1], n) @ w
+        return y
+    y = np.zeros((x.shape[n], R))
+    for k0, k1 in _slab_ranges(last, chunk):
+        om = list(omegas)
+        om[d - 1] = np.asarray(omegas[d - 1])[k0:k1]
+        y += unfold(x[..., k0:k1], n) @ kr_for_mode(om, n)
+    return y
+
+
+def sketch_all_modes(x: np.ndarray, omegas: Sequence[np.ndarray], chunk: Optional[int] = None) -> List[np.ndarray]:
+    """Memoized sketches: one shared set {Omega_k} reused for every mode."""
+    return [sketch_mode(x, omegas, n, chunk) for n in range(x.ndim)]
+
+
+def sketch_mode_rows(flat: np.ndarray, dims: Sequence[int], omegas: Sequence[np.ndarray], n: int,
+                     rows: Sequence[int]) -> np.ndarray:
+    """Rows ``rows`` of Y_n only (sampled full-size parity): Y_n(i,:) = X_(n)(i,:) · KR_n,
+    with X_(n)(i,:) gathered from the fp32 buffer one last-mode slab at a time."""
+    dims = tuple(int(v) for v in dims)
+    d = len(dims)
+    R = np.asarray(omegas[(n + 1) % d]).shape[1]
+    inner = int(np.prod(dims[:-1]))
+    out = np.zeros((len(rows), R))
+    if n == d - 1:
+        w = kr_for_mode(omegas, n)
+        for t, i in enumerate(rows):
+            out[t] = np.asarray(flat[i * inner:(i + 1) * inner], dtype=np.float64) @ w
+        return out
+    w_in = kr_for_mode([o for o in omegas[:-1]] + [np.ones((1, R))], n)  # modes < d except n
+    for k in range(dims[-1]):
+        slab = as_tensor(flat[k * inner:(k + 1) * inner], dims[:-1])
+        xu = unfold(slab, n)  # I_n x prod_{m<d-1, m!=n} I_m
+        for t, i in enumerate(rows):
+            out[t] += (xu[i] @ w_in) * np.asarray(omegas[d - 1][k], dtype=np.float64)
+    return out
+
+
+# ----------------------------------------------------------------- orthonormalisation, TTM
+def thin_qr(y: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
+    """Thin QR Y = Q R (Alg. 1 line 3; Alg. 7 line 4) by Householder
+    (LAPACK geqrf via numpy), columns signed so that diag(R) > 0 (the unique Q of a
+    full-rank Y, the one CholeskyQR also produces)."""
+    q, r = np.linalg.qr(np.asarray(y, dtype=np.float64), mode="reduced")
+    s = np.sign(np.diag(r))
+    s[s == 0] = 1.0
+    return q * s[None, :], r * s[:, None]
+
+
+def ttm(x: np.ndarray, a: np.ndarray, n: int) -> np.ndarray:
+    """Tensor-times-matrix Y = X ×_n A, i.e. Y_(n) = A X_(n)."""
+    dims = list(x.shape)
+    dims[n] = a.shape[0]
+    return fold(np.asarray(a, dtype=np.float64) @ unfold(x, n), n, dims)
+
+
+def multi_ttm(x: np.ndarray, mats: Sequence[Optional[np.ndarray]]) -> np.ndarray:
+    """X ×_1 A_1 ×_2 ... ×_d A_d, applied in ascending mode order (None = identity)."""
+    y = x
+    for n, a in enumerate(mats):
+        if a is not None:
+            y = ttm(y, a, n)
+    return y
+
+
+def leading_left_singular_vectors(m: np.ndarray, r: int) -> Tuple[np.ndarray, np.ndarray]:
+    """U(:, 1:r) and the singular values of M (LAPACK SVD), Alg. 2 line 2-3 pattern."""
+    u, s, _ = np.linalg.svd(np.asarray(m, dtype=np.float64), full_matrices=False)
+    return u[:, :r], s
+
+
+# ----------------------------------------------------------------- Tucker algorithms
+def _core_slabwise(x: np.ndarray, qs: Sequence[np.ndarray], chunk: Optional[int]) -> np.ndarray:
+    """G = X ×_1 Q_1ᵀ ×_2 ... ×_d Q_dᵀ (Alg. 7 line 6), last-mode slabs summed."""
+    d = x.ndim
+    g = None
+    for k0, k1 in _slab_ranges(x.shape[-1], chunk):
+        mats = [q.T for q in qs[:-1]] + [qs[-1][k0:k1].T]
+        part = multi_ttm(x[..., k0:k1], mats)
+        g = part if g is None else g + part
+    return g
+
+
+def reconstruct(core: np.ndarray, qs: Sequence[np.ndarray]) -> np.ndarray:
+    """X̂ = G ×_1 Q_1 ×_2 ... ×_d Q_d."""
+    return multi_ttm(core, list(qs))
+
+
+def tucker_error(x: np.ndarray, core: np.ndarray, qs: Sequence[np.ndarray], chunk: Optional[int] = None) -> float:
+    """||X - X̂||_F / ||X||_F, X̂ rebuilt slab by slab."""
+    num = 0.0
+    den = 0.0
+    for k0, k1 in _slab_ranges(x.shape[-1], chunk):
+        xh = multi_ttm(core, list(qs[:-1]) + [qs[-1][k0:k1]])
+        diff = x[..., k0:k1] - xh
+        num += float(np.sum(diff * diff))
+        den += float(np.sum(x[..., k0:k1] ** 2))
+    return float(np.sqrt(num / den))
+
+
+def rhosvd(x: np.ndarray, omegas: Sequence[np.ndarray], ranks: Sequence[int], chunk: Optional[int] = None,
+           with_error: bool = True):
+    """RHOSVD-KRP-MEMO (Alg. 7 with memoization) + truncation R4.
+
+    1. Y_n = MTTKRP with the shared {Omega_k}       for every n
+    2. Q_n = thin QR of Y_n, diag(R) > 0                    (l_n = R columns)
+    3. G = X ×_1 Q_1ᵀ ... ×_d Q_dᵀ
+    4. if r_n < l_n: U_n = leading r_n left singular vectors of G_(n) (Alg. 2 pattern
+       P:118-120 applied to the core, S:371 recompression); Q_n <- Q_n U_n;
+       G <- G ×_n U_nᵀ  (modes in ascending order, each on the current G)
+    5. relative error ||X - [G; Q]|| / ||X||
+    Returns (qs, core, err, ys)."""
+    d = x.ndim
+    ys = sketch_all_modes(x, omegas, chunk)
+    qs = [thin_qr(y)[0] for y in ys]
+    g = _core_slabwise(x, qs, chunk)
+    for n in range(d):
+        r = int(ranks[n])
+        if r < qs[n].shape[1]:
+            u, _ = leading_left_singular_vectors(unfold(g, n), r)
+            qs[n] = qs[n] @ u
+            g = ttm(g, u.T, n)
+    err = tucker_error(x, g, qs, chunk) if with_error else None
+    return qs, g, err, ys
+
+
+def sthosvd(x: np.ndarray, om_steps: Sequence[Sequence[Optional[np.ndarray]]], ranks: Sequence[int],
+            with_error: bool = True):
+    """RSTHOSVD-KRP (Alg. 8) with per-step truncation (R4, R5, R6).
+
+    G^(0) = X.  For i = 1..d (ascending):
+      1. Y_i = G_(i) (Omega ⊙ ... without i) with step-i Omegas; for an already
+         compressed mode j < i only the leading r_j rows of Omega_j are used (R5)
+      2. Q = thin QR(Y_i)
+      3. B = G ×_i Qᵀ
+      4. U = leading r_i left singular vectors of B_(i) (Alg. 2 pattern)
+      5. G <- B ×_i Uᵀ ; Q_i = Q U
+    Returns (qs, core, err, ys) where ys[i] is the step-i sketch."""
+    d = x.ndim
+    g = x
+    qs = []
+    ys = []
+    for i in range(d):
+        om = []
+        for j in range(d):
+            if j == i:
+                om.append(None)
+            else:
+                om.append(np.asarray(om_steps[i][j], dtype=np.float64)[: g.shape[j]])
+        om[i] = np.ones((1, np.asarray(om_steps[i][(i + 1) % d]).shape[1]))  # placeholder, unused
+        y = sketch_mode(g, om, i)
+        ys.append(y)
+        q, _ = thin_qr(y)
+        b = ttm(g, q.T, i)
+        r = int(ranks[i])
+        if r < q.shape[1]:
+            u, _ = leading_left_singular_vectors(unfold(b, i), r)
+            q = q @ u
+            b = ttm(b, u.T, i)
+        g = b
+        qs.append(q)
+    err = tucker_error(x, g, qs) if with_error else None
+    return qs, g, err, ys
+
+
+# ----------------------------------------------------------------- accounting
+def sketch_flops(dims: Sequence[int], R: int, all_modes: bool = True) -> int:
+    """Algorithmic sketch flops: 4·N·R memoized all-modes (Table 1
+    reading R8), 2·N·R for one mode."""
+    N = int(np.prod(dims, dtype=np.int64))
+    return (4 if all_modes else 2) * N * int(R)
