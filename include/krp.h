@@ -1,0 +1,157 @@
+/*
+ * krp.h — C ABI of the B200-native Khatri-Rao random-projection (KRP) sketch
+ * library (libkrp.so) for randomized HOSVD / STHOSVD, arXiv 2507.23207.
+ *
+ * The hot path is the MTTKRP sketch of a dense d-way tensor against Gaussian
+ * factors (Alg. 7 line 3; memoized form P:571-574):
+ *
+ *     Y_n = X_(n) (Omega_d ⊙ ... ⊙ Omega_{n+1} ⊙ Omega_{n-1} ⊙ ... ⊙ Omega_1)
+ *
+ * Conventions for every entry point
+ * ---------------------------------
+ * - X is fp32, first-index-fastest: element (i_1..i_d) (0-based) lives at
+ *   offset sum_k i_k * prod_{m<k} I_m (the same bytes as a
+ *   C-contiguous array of shape (I_d, ..., I_1)).  The mode-n unfolding X_(n)
+ *   takes its columns in that order with mode n removed, which is the
+ *   row order of the Khatri-Rao product above (reading R1 in DESIGN.md).
+ * - Omega_k is fp32, row-major I_k x R (element (i, r) at i*R + r).
+ * - Y_n, Q_n are fp32 row-major I_n x R (resp. I_n x r_n).
+ * - The core G is fp32, first-index-fastest, dims (r_1..r_d).
+ * - Unless a name ends in _host, every array pointer is a DEVICE pointer owned
+ *   by the caller; the library never frees or retains it past the call.  Arrays
+ *   of pointers (omega, Y, Q) are HOST arrays of d device pointers.
+ * - `stream` is a cudaStream_t (NULL = legacy default stream).  Work is
+ *   enqueued on it; results are stream-ordered.  Functions that return a host
+ *   scalar (rel_err) synchronize the stream before returning.
+ * - `ws`/`ws_bytes`: device workspace of at least krp_workspace_bytes(...)
+ *   bytes, 256-byte aligned.  ws == NULL makes the library allocate (and free)
+ *   the workspace itself with stream-ordered cudaMallocAsync.
+ * - Results are deterministic for a fixed configuration and device: every
+ *   cross-block sum is a fixed-order reduction (no floating-point atomics).
+ *
+ * Errors: every function returns a krp_status.  Arguments are validated before
+ * anything is launched; on error, outputs are unspecified.  krp_status_string()
+ * gives a description; krp_last_error_message() gives details of the last error
+ * on the calling thread.  No C++ exception crosses this boundary.
+ */
+#ifndef KRP_H_
+#define KRP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__) || defined(__clang__)
+#define KRP_API __attribute__((visibility("default")))
+#else
+#define KRP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum krp_status {
+  KRP_OK = 0,
+  KRP_EINVAL = 1,       /* null pointer, d not in [2,8], R not in [1,128], dim < 1, n out of range */
+  KRP_ESHAPE = 2,       /* r_n > R, R > min(I_n, N/I_n), inconsistent slab geometry */
+  KRP_ECUDA = 3,        /* a CUDA runtime / launch error */
+  KRP_ENCCL = 4,        /* NCCL unavailable or a collective failed */
+  KRP_ENUMERIC = 5,     /* CholeskyQR failed even after the shifted fallback */
+  KRP_ENOMEM = 6,       /* ws_bytes < krp_workspace_bytes(...) or allocation failed */
+  KRP_EUNSUPPORTED = 7  /* no kernel for this device (requires sm_100a) */
+} krp_status;
+
+/* op codes for krp_workspace_bytes */
+enum {
+  KRP_OP_SKETCH_ALL = 0,
+  KRP_OP_SKETCH_MODE = 1,
+  KRP_OP_RHOSVD = 2,
+  KRP_OP_STHOSVD = 3,
+  KRP_OP_SKETCH_ALL_HOST = 4, /* krp_sketch_all_modes_host: includes device copies of X, Omega, Y */
+  KRP_OP_RHOSVD_ERR = 5       /* krp_rhosvd with rel_err != NULL */
+};
+
+/* Sketch engine selection (krp_set_engine); default KRP_ENGINE_AUTO. */
+enum {
+  KRP_ENGINE_AUTO = 0, /* tcgen05 3xTF32 kernel where the shape is supported, else SIMT */
+  KRP_ENGINE_TC = 1,   /* force the tcgen05 kernel (KRP_EUNSUPPORTED if the shape is not supported) */
+  KRP_ENGINE_SIMT = 2  /* force the fp32 CUDA-core kernel */
+};
+
+KRP_API const char* krp_status_string(int status);
+KRP_API const char* krp_last_error_message(void);
+KRP_API int krp_version(void);
+KRP_API int krp_set_engine(int engine);
+
+/* Workspace size in bytes for `op` (one of KRP_OP_*).  ranks may be NULL for the sketch ops. */
+KRP_API size_t krp_workspace_bytes(int op, int d, const int64_t* dims, int R, const int* ranks);
+
+/* All-mode memoized sketch: one shared set {Omega_k}, every Y_n.
+ * omega[k]: I_k x R; Y[n]: I_n x R (outputs).  Algorithmic work 4*N*R flops. */
+KRP_API int krp_sketch_all_modes(const float* X, int d, const int64_t* dims, const float* const* omega, int R,
+                         float* const* Y, void* ws, size_t ws_bytes, void* stream);
+
+/* Same, with HOST buffers (X, omega[k], Y[n] in host memory, ideally pinned): copies
+ * host->device, sketches, copies device->host, all on `stream`, and synchronizes.
+ * ws must hold krp_workspace_bytes(KRP_OP_SKETCH_ALL_HOST, ...) bytes (or be NULL). */
+KRP_API int krp_sketch_all_modes_host(const float* X_host, int d, const int64_t* dims, const float* const* omega_host,
+                              int R, float* const* Y_host, void* ws, size_t ws_bytes, void* stream);
+
+/* Single-mode sketch Y = X_(n) (⊙_{k!=n} Omega_k) (Alg. 7 line 3 / Alg. 8 line 4).
+ * n is 0-based; omega[n] is not read (may be NULL).  2*N*R flops. */
+KRP_API int krp_sketch_mode(const float* X, int d, const int64_t* dims, int n, const float* const* omega, int R, float* Y,
+                    void* ws, size_t ws_bytes, void* stream);
+
+/* RHOSVD-KRP-MEMO (Alg. 7 with memoization):
+ *   Y_n = memoized sketch; Q_n = CholeskyQR2(Y_n) (thin QR with diag(R) > 0);
+ *   G = X x_1 Q_1^T ... x_d Q_d^T; then, for r_n < R, truncation by HOSVD of the
+ *   small core (reading R4): U_n = leading r_n left singular vectors of G_(n),
+ *   Q_n <- Q_n U_n, G <- G x_n U_n^T.
+ * ranks[n] = r_n in [1, R]; Q[n]: I_n x r_n; core: prod r_n.
+ * rel_err (host, nullable): if non-NULL, ||X - [G; Q]||_F / ||X||_F is computed with one more
+ * pass over X (needs krp_workspace_bytes(KRP_OP_RHOSVD_ERR, ...)) and the stream is synchronized. */
+KRP_API int krp_rhosvd(const float* X, int d, const int64_t* dims, const int* ranks, int R, const float* const* omega,
+               float* const* Q, float* core, double* rel_err, void* ws, size_t ws_bytes, void* stream);
+
+/* RSTHOSVD-KRP (Alg. 8), modes in ascending order, per-step truncation (R4):
+ *   for i: Y = G_(i) (⊙_{j!=i} Omega^{(i)}_j); Q = CholeskyQR2(Y); B = G x_i Q^T;
+ *          U = leading r_i left singular vectors of B_(i); G <- B x_i U^T; Q_i = Q U.
+ * omega[i*d + j] (host array of d*d device pointers): step i, mode j, I_j x R; entries with
+ * j == i are not read.  For j < i only the leading r_j rows are read (reading R5). */
+KRP_API int krp_sthosvd(const float* X, int d, const int64_t* dims, const int* ranks, int R, const float* const* omega,
+                float* const* Q, float* core, double* rel_err, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------ multi-GPU (slab sharding)
+ * The tensor is split into contiguous slabs along its LAST mode (contiguous in memory).  Each
+ * rank passes its local slab X (dims[d-1] = local slab length) plus the global last-mode size and
+ * the slab offset; omega[d-1] is the GLOBAL I_d x R factor.  Outputs are global and replicated on
+ * every rank.  Collectives (NCCL over NVLink) are issued on `stream`. */
+typedef struct krp_comm_s* krp_comm;
+
+/* Size of the opaque unique id (bytes).  Rank 0 creates it, the caller broadcasts it
+ * (e.g. with torch.distributed), every rank passes it to krp_comm_init. */
+KRP_API size_t krp_comm_id_bytes(void);
+KRP_API int krp_comm_get_unique_id(void* id_out);
+KRP_API int krp_comm_init(krp_comm* comm, int nranks, int rank, const void* id);
+KRP_API int krp_comm_destroy(krp_comm comm);
+
+KRP_API int krp_sketch_all_modes_dist(const float* X_slab, int d, const int64_t* dims_local, int64_t I_d_global,
+                              int64_t slab_begin, const float* const* omega, int R, float* const* Y, void* ws,
+                              size_t ws_bytes, krp_comm comm, void* stream);
+KRP_API int krp_rhosvd_dist(const float* X_slab, int d, const int64_t* dims_local, int64_t I_d_global, int64_t slab_begin,
+                    const int* ranks, int R, const float* const* omega, float* const* Q, float* core,
+                    double* rel_err, void* ws, size_t ws_bytes, krp_comm comm, void* stream);
+/* Workspace for the _dist calls: krp_workspace_bytes(op, d, dims_local, R, ranks) with the global
+ * last-mode size passed through this helper. */
+KRP_API size_t krp_workspace_bytes_dist(int op, int d, const int64_t* dims_local, int64_t I_d_global, int R,
+                                const int* ranks);
+
+/* Device-side launch counter (number of kernels this library launched since the last reset),
+ * for the bench's gpu_launches field. */
+KRP_API uint64_t krp_launch_count(void);
+KRP_API void krp_reset_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KRP_H_ */

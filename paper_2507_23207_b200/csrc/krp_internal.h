@@ -1,0 +1,50 @@
+// krp_internal.h — internal entry points between the translation units of libkrp.
+#pragma once
+#include "krp_common.cuh"
+
+namespace krp {
+
+// ---- sketch engines
+size_t simt_sketch_ws_bytes(const Dims& g, int n, int R);
+int simt_sketch_mode(const float* X, const Dims& g, int n, const OmegaPtrs& om, int R, float* Y, Arena& ar,
+                     cudaStream_t s);
+
+// tcgen05 3xTF32 engine.  want_mode[k] selects which Y_k are produced.  Returns
+// KRP_EUNSUPPORTED (without launching) when the shape/device is not supported.
+bool tc_sketch_supported(const Dims& g, int R, const bool* want_mode);
+size_t tc_sketch_ws_bytes(const Dims& g, int R, const bool* want_mode);
+int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const bool* want_mode, float* const* Y,
+              Arena& ar, cudaStream_t s);
+
+// Dispatch over engines (krp_set_engine); Y[k] for every k with want_mode[k].
+size_t sketch_ws_bytes(const Dims& g, int R, const bool* want_mode);
+int sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const bool* want_mode, float* const* Y,
+           Arena& ar, cudaStream_t s);
+
+// ---- dense linear algebra (krp_linalg.cu)
+// CholeskyQR with shifted first pass and two refinement passes (sCholeskyQR3; plain CholeskyQR2
+// when the first Cholesky succeeds without shift).  Y: rows x R fp32 row-major.
+// Writes Q (rows x R) as fp32 (Qf, may be null) and fp64 (Qd, may be null).
+size_t cholqr_ws_bytes(int64_t rows, int R);
+int cholqr(const float* Y, int64_t rows, int R, float* Qf, double* Qd, int* flag_dev, Arena& ar, cudaStream_t s);
+
+// Y = X x_n A for X of dims g (fp32), A: J x I_n with element (j, i) at A[j*sj + i*si] (fp32).
+int ttm(const float* X, const Dims& g, int n, const float* A, int J, int64_t sj, int64_t si, float* Y,
+        cudaStream_t s);
+
+// H = T_(n) T_(n)^T (J x J, fp64) for T of dims g with J = g.n[n].
+size_t mode_gram_ws_bytes(const Dims& g, int n);
+int mode_gram(const float* T, const Dims& g, int n, double* H, Arena& ar, cudaStream_t s);
+
+// Leading r eigenvectors (descending eigenvalues) of a symmetric J x J fp64 matrix (J <= 64),
+// written as U (J x r row-major) in fp32.
+int sym_eig_top(const double* H, int J, int r, float* U, cudaStream_t s);
+
+// sum (X - Xh)^2 and sum X^2 over n elements, fp64, fixed order; out[0], out[1] accumulate (+=).
+size_t sqdiff_ws_bytes(int64_t n);
+int sqdiff_accumulate(const float* X, const float* Xh, int64_t n, double* out, Arena& ar, cudaStream_t s);
+
+// row-major matrix copy with column subset: dst[i*dcols + j] = src[i*scols + j], j < dcols
+int copy_cols(const float* src, int64_t rows, int scols, float* dst, int dcols, cudaStream_t s);
+
+}  // namespace krp
