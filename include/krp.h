@@ -146,6 +146,14 @@ KRP_API int krp_rhosvd_dist(const float* X_slab, int d, const int64_t* dims_loca
 KRP_API size_t krp_workspace_bytes_dist(int op, int d, const int64_t* dims_local, int64_t I_d_global, int R,
                                 const int* ranks);
 
+/* Kernel-level profiling of the dominant sketch kernel: when enabled, the library records CUDA
+ * events around every launch of the main sketch kernel (tcgen05 or SIMT) on the caller's stream.
+ * krp_profile_read synchronizes those events and returns the summed duration (ms), the number of
+ * launches and the algorithmic bytes/flops those launches processed. */
+KRP_API int krp_profile_enable(int on);
+KRP_API int krp_profile_read(double* kernel_ms, uint64_t* launches, double* alg_bytes, double* alg_flops);
+KRP_API void krp_profile_reset(void);
+
 /* Device-side launch counter (number of kernels this library launched since the last reset),
  * for the bench's gpu_launches field. */
 KRP_API uint64_t krp_launch_count(void);

@@ -18,6 +18,7 @@ from typing import List, Optional, Sequence, Tuple
 import torch
 
 __all__ = [
+    "krp_profile_enable", "krp_profile_read", "krp_profile_reset",
     "lib", "KrpError", "OP_SKETCH_ALL", "OP_SKETCH_MODE", "OP_RHOSVD", "OP_STHOSVD", "OP_SKETCH_ALL_HOST",
     "OP_RHOSVD_ERR", "ENGINE_AUTO", "ENGINE_TC", "ENGINE_SIMT", "krp_set_engine", "krp_workspace_bytes",
     "krp_sketch_all_modes", "krp_sketch_all_modes_host", "krp_sketch_mode", "krp_rhosvd", "krp_sthosvd",
@@ -35,7 +36,7 @@ EXPORTED_SYMBOLS = [
     "krp_sketch_all_modes", "krp_sketch_all_modes_host", "krp_sketch_mode", "krp_rhosvd", "krp_sthosvd",
     "krp_comm_id_bytes", "krp_comm_get_unique_id", "krp_comm_init", "krp_comm_destroy",
     "krp_sketch_all_modes_dist", "krp_rhosvd_dist", "krp_workspace_bytes_dist", "krp_launch_count",
-    "krp_reset_launch_count",
+    "krp_reset_launch_count", "krp_profile_enable", "krp_profile_read", "krp_profile_reset",
 ]
 
 _lib = None
@@ -87,6 +88,9 @@ def lib() -> ctypes.CDLL:
         l_.krp_rhosvd_dist.argtypes = [_P, ctypes.c_int, _I64P, ctypes.c_int64, ctypes.c_int64, _IP, ctypes.c_int,
                                        ptrs, ptrs, _P, ctypes.POINTER(ctypes.c_double), _P, ctypes.c_size_t, _P, _P]
         l_.krp_launch_count.restype = ctypes.c_uint64
+        l_.krp_profile_enable.argtypes = [ctypes.c_int]
+        l_.krp_profile_read.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64),
+                                        ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
         _lib = l_
     return _lib
 
@@ -149,6 +153,22 @@ def krp_launch_count() -> int:
 
 def krp_reset_launch_count() -> None:
     lib().krp_reset_launch_count()
+
+
+def krp_profile_enable(on: bool = True) -> None:
+    _check(lib().krp_profile_enable(1 if on else 0), "krp_profile_enable")
+
+
+def krp_profile_reset() -> None:
+    lib().krp_profile_reset()
+
+
+def krp_profile_read():
+    """(kernel_ms total, launches, algorithmic bytes, algorithmic flops) of the dominant sketch kernel."""
+    ms, n, b, f = ctypes.c_double(), ctypes.c_uint64(), ctypes.c_double(), ctypes.c_double()
+    _check(lib().krp_profile_read(ctypes.byref(ms), ctypes.byref(n), ctypes.byref(b), ctypes.byref(f)),
+           "krp_profile_read")
+    return ms.value, int(n.value), b.value, f.value
 
 
 # ------------------------------------------------------------------ entry points

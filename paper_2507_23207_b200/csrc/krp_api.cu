@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <cstdarg>
 #include <cstring>
 #include <vector>
@@ -29,6 +30,33 @@ static std::atomic<uint64_t> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n)); }
 
 static std::atomic<int> g_engine{KRP_ENGINE_AUTO};
+
+// ---- kernel profiling
+struct ProfRec {
+  cudaEvent_t a, b;
+  double bytes, flops;
+};
+static std::mutex g_prof_mu;
+static std::vector<ProfRec> g_prof;
+static std::atomic<int> g_prof_on{0};
+static cudaEvent_t g_prof_pending = nullptr;
+bool prof_on() { return g_prof_on.load() != 0; }
+void prof_begin(cudaStream_t s) {
+  if (!prof_on()) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  cudaEventCreate(&g_prof_pending);
+  cudaEventRecord(g_prof_pending, s);
+}
+void prof_end(cudaStream_t s, double bytes, double flops) {
+  if (!prof_on()) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (!g_prof_pending) return;
+  cudaEvent_t b;
+  cudaEventCreate(&b);
+  cudaEventRecord(b, s);
+  g_prof.push_back(ProfRec{g_prof_pending, b, bytes, flops});
+  g_prof_pending = nullptr;
+}
 
 // ------------------------------------------------------------------ validation
 static int validate_common(const void* X, int d, const int64_t* dims, int R) {
@@ -629,6 +657,38 @@ int krp_set_engine(int engine) {
   return KRP_OK;
 }
 uint64_t krp_launch_count(void) { return krp::g_launches.load(); }
+
+int krp_profile_enable(int on) {
+  krp::g_prof_on.store(on ? 1 : 0);
+  return KRP_OK;
+}
+
+void krp_profile_reset(void) {
+  std::lock_guard<std::mutex> lk(krp::g_prof_mu);
+  for (auto& r : krp::g_prof) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  krp::g_prof.clear();
+}
+
+int krp_profile_read(double* kernel_ms, uint64_t* launches, double* alg_bytes, double* alg_flops) {
+  std::lock_guard<std::mutex> lk(krp::g_prof_mu);
+  double ms = 0.0, by = 0.0, fl = 0.0;
+  for (auto& r : krp::g_prof) {
+    KRP_CHECK_CUDA(cudaEventSynchronize(r.b));
+    float t = 0.f;
+    KRP_CHECK_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    ms += t;
+    by += r.bytes;
+    fl += r.flops;
+  }
+  if (kernel_ms) *kernel_ms = ms;
+  if (launches) *launches = krp::g_prof.size();
+  if (alg_bytes) *alg_bytes = by;
+  if (alg_flops) *alg_flops = fl;
+  return KRP_OK;
+}
 void krp_reset_launch_count(void) { krp::g_launches.store(0); }
 
 static size_t ws_bytes_impl(int op, int d, const int64_t* dims, int64_t Id_global, int R, const int* ranks) {

@@ -46,6 +46,11 @@ const char* last_error();
 // Launch counter (krp_launch_count).
 void count_launch(int n = 1);
 
+// Kernel profiling (krp_profile_*): prof_begin/prof_end bracket one launch of the dominant kernel.
+bool prof_on();
+void prof_begin(cudaStream_t s);
+void prof_end(cudaStream_t s, double alg_bytes, double alg_flops);
+
 #define KRP_CHECK_CUDA(expr)                                                        \
   do {                                                                              \
     cudaError_t e__ = (expr);                                                       \

@@ -9,6 +9,8 @@
 // memory), each warp streams a quarter of those columns, per-thread fp32
 // accumulators; the 4 warps are combined in a fixed order and every block writes a
 // partial I_n x RC tile.  A second kernel sums the partials in fp64, fixed order.
+#include <algorithm>
+
 #include "krp_common.cuh"
 #include "krp_internal.h"
 
@@ -134,6 +136,7 @@ int simt_sketch_mode(const float* X, const Dims& g, int n, const OmegaPtrs& om, 
   for (int pass = 0; pass < p.passes; ++pass) {
     const int r0 = pass * p.RC;
     dim3 grid(static_cast<unsigned>(p.row_tiles), static_cast<unsigned>(p.P));
+    prof_begin(s);
     switch (p.RC) {
       case 16:
         sketch_mode_simt_kernel<16><<<grid, 128, 0, s>>>(X, g, n, om, R, r0, p.ncols, p.cols_per_chunk, partial);
@@ -146,6 +149,8 @@ int simt_sketch_mode(const float* X, const Dims& g, int n, const OmegaPtrs& om, 
         break;
     }
     KRP_CHECK_LAUNCH();
+    // algorithmic work of this launch: one read of X, 2*N*RC flops of the single-mode MTTKRP
+    prof_end(s, 4.0 * static_cast<double>(g.N), 2.0 * static_cast<double>(g.N) * std::min(p.RC, R - r0));
     const int64_t tot = g.n[n] * p.RC;
     reduce_partials_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(partial, p.P, g.n[n], p.RC, R,
                                                                                      r0, Y);
