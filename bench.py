@@ -60,57 +60,50 @@ def _workload(cfg, world):
 
 # ------------------------------------------------------------------ clocks (nvidia-smi during the timed region)
 class ClockSampler:
-    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.active",
-              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
-              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+    """SM clock + throttle reasons polled through NVML (~1 ms) during the timed region; falls back to
+    `nvidia-smi -lms 200` when NVML is unavailable."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
-        self.lines = []
-        self.proc = None
+        self.samples = []
+        self.stop_ev = threading.Event()
+        self.th = None
+        self.smax = None
+
+    def _poll(self):
+        import pynvml
+        h = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
+        self.smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        while not self.stop_ev.is_set():
+            try:
+                clk = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((clk, rs))
+            except Exception:
+                pass
+            time.sleep(0.001)
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.idx}", "--query-gpu=" + ",".join(self.FIELDS),
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.th = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self.th = threading.Thread(target=self._poll, daemon=True)
             self.th.start()
-        except (OSError, FileNotFoundError):
-            self.proc = None
-
-    def _read(self):
-        for ln in self.proc.stdout:
-            self.lines.append(ln.strip())
+        except Exception:
+            self.th = None
 
     def stop(self):
-        if self.proc is None:
+        if self.th is None:
             return None
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
+        self.stop_ev.set()
         self.th.join(timeout=2)
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                smax.append(float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[4:8]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        if not sm:
+        if not self.samples:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        reasons = sorted({nm for _, rs in self.samples for nm, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": statistics.median(c for c, _ in self.samples), "sm_max_mhz": self.smax,
+                "reasons": reasons, "samples": len(self.samples), "source": "nvml"}
 
 
 # ------------------------------------------------------------------ CPU oracle baseline
@@ -136,9 +129,21 @@ def _cores():
     return nt
 
 
+def _calibrate_slabs(cfg, seed, om, target_s):
+    """Number of last-mode slabs whose oracle sketch takes about target_s (doubling calibration)."""
+    slabs, t = 1, 0.0
+    while slabs < cfg.dims[-1]:
+        t, _ = _oracle_sample(cfg, seed, slabs, om)
+        if t >= 0.25 * target_s:
+            break
+        slabs = min(cfg.dims[-1], slabs * 2)
+    if t > 0:
+        slabs = int(max(1, min(cfg.dims[-1], slabs * target_s / t)))
+    return slabs
+
+
 def cpu_baseline(cfg, seed, om, target_s=12.0):
-    t1, f1 = _oracle_sample(cfg, seed, 1, om)
-    slabs = int(max(1, min(cfg.dims[-1], target_s / max(t1, 1e-3))))
+    slabs = _calibrate_slabs(cfg, seed, om, target_s)
     t, f = _oracle_sample(cfg, seed, slabs, om)
     return {"value": f / t / 1e12, "unit": "TFLOP/s", "cores": _cores(), "kind": "oracle",
             "sample": f"fp64 numpy explicit-KR all-mode sketch of last-mode slabs [0,{slabs}) of {cfg.name} "
@@ -150,10 +155,9 @@ def run_reference(args, cfg, rank, world):
     if rank != 0:
         return 0
     om = synth.omegas(cfg.dims, cfg.R, args.seed)
-    t1, _ = _oracle_sample(cfg, args.seed, 1, om)
     budget = 150.0
     per_step = budget / max(1, args.steps + args.warmup)
-    slabs = int(max(1, min(cfg.dims[-1], per_step / max(t1, 1e-3))))
+    slabs = _calibrate_slabs(cfg, args.seed, om, per_step)
     for _ in range(args.warmup):
         _oracle_sample(cfg, args.seed, slabs, om)
     times, flops = [], 0

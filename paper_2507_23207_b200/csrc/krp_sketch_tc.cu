@@ -23,8 +23,8 @@
 // T(s) = Σ_lanes z1·W_L by a warp-shuffle transposed reduction + a fixed-order cross-warp sum.
 // A second kernel (fixed order) sums the per-CTA partials and applies the multi-TTVs.
 //
-// Warp roles (448 threads): 0-3 split (TMEM lane quarters 0-3), 4-11 epilogue (two r-halves
-// per lane quarter), 12 TMA producer, 13 MMA issuer.
+// Warp roles (704 threads): 0-3 split (TMEM lane quarters 0-3), 4-19 epilogue ((P|Q side) x
+// (r-half) x lane quarter), 20 TMA producer, 21 MMA issuer.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -40,12 +40,14 @@ namespace krp {
 namespace {
 using namespace sm100;
 
-constexpr int kThreads = 448;
-constexpr int kEpiWarp0 = 4;
-constexpr int kNumEpiWarps = 8;
-constexpr int kTmaWarp = 12;
-constexpr int kMmaWarp = 13;
-constexpr int kCH = 16;             // TMEM A-chunk width (K columns per staged operand copy)
+constexpr int kSplitPar = 1;       // split warps per TMEM lane quarter (chunk parities)
+constexpr int kNumSplitWarps = 4 * kSplitPar;
+constexpr int kEpiWarp0 = kNumSplitWarps;
+constexpr int kNumEpiWarps = 8;    // (P | Q side) x TMEM lane quarter
+constexpr int kTmaWarp = kEpiWarp0 + kNumEpiWarps;
+constexpr int kMmaWarp = kTmaWarp + 1;   // issues the P-GEMM MMAs (and owns the TMEM allocation)
+constexpr int kMmaWarpQ = kMmaWarp + 1;  // issues the Q-GEMM MMAs
+constexpr int kThreads = (kMmaWarpQ + 1) * 32;
 constexpr int kTile = 128;
 constexpr int kStageFloats = 4 * 128 * 32;  // one 128x128 fp32 tile = 4 TMA boxes of {32, 128}
 constexpr int kMaxTcR = 64;
@@ -54,40 +56,103 @@ struct TcParams {
   int64_t M, C, S;
   int RB, CB;
   int64_t T;
-  int R, NP, N2;
+  int R, NP, N2, R8;  // NP: B-image rows; R8 = round8(R): row of B_lo / column of the hi·lo accumulator
+  int triple;         // 1: three N=N2 MMAs into one accumulator (hh + hl + lh); 0: [hi|lo] concat (N=NP) + lo·hi
+  int DN;             // accumulator columns per side (NP for concat, N2 for triple)
+  int RS;             // row stride (floats) of the OmS table: round4(R), a row is a 16 B-multiple bulk copy
   int NS, NC, NA;
   int do_p, do_q, do_t;
-  int maxseg;
-  int tm_acc, tm_chunk;
-  uint32_t sm_x, sm_bp, sm_bq, sm_red, sm_bar;
-  int m, m2, d;
-  int64_t n[kMaxD];
-  int64_t gs[kMaxD];  // stride of mode k inside its group (rows / cols / slices)
-  const float* om[kMaxD];
-  float* partA1;  // [nslot][128][R]
+  int maxseg;  // max number of CTAs contributing to one (rb, cb) pair: partial slot = pair*maxseg + k
+  int tm_acc, tm_chunk, tm_a;  // TMEM columns: accumulator stages, A-operand chunk stages, A1/A2
+  uint32_t sm_x, sm_bp, sm_bq, sm_red, sm_bar, sm_ws;
+  float* partA1;  // [npairs*maxseg][128][R]
   float* partA2;
   int* slot_pair;  // [nslot]
   float* Tpart;    // [RB*CB][S][R]
-  const float* WL;   // [M][R]  Khatri-Rao rows of the row modes
-  const float* WR;   // [C][R]  Khatri-Rao rows of the col modes
-  const float* OmS;  // [S][R]  Khatri-Rao rows of the slice modes
-  int dbg;           // development bottleneck probes (KRP_TC_DEBUG): 0 normal, 1 TMA only,
-                     // 2 TMA + split, 3 TMA + split + MMA (no epilogue)
+  const float* BPimg;  // [CB][NP*128]: W_R rows of col block cb, already in the SMEM B-operand layout
+  const float* BQimg;  // [RB][NP*128]: W_L rows of row block rb
+  const float* OmS;    // [S][RS]: Khatri-Rao rows of the slice modes
+  long long* trace;    // development timeline (KRP_TC_TRACE): CTA 0 role timestamps, null in production
+  int dbg;             // development bottleneck probes (KRP_TC_DEBUG): 0 normal, 1 TMA only,
+                       // 2 TMA + split, 3 TMA + split + MMA (no epilogue), 4 TMA self-consumed
 };
 
-__device__ __forceinline__ float omega_prod(const TcParams& p, int k0, int k1, int64_t lin, int r) {
-  // Π_{k in [k0,k1)} Ω_k(i_k(lin), r), lin = linear index inside that mode group
-  float w = 1.f;
-  for (int k = k0; k < k1; ++k) {
-    const int64_t ik = (lin / p.gs[k]) % p.n[k];
-    w *= __ldg(p.om[k] + ik * p.R + r);
-  }
-  return w;
+// floor(num / den) for 0 <= num < 2^62, den > 0, without the 64-bit integer division routine
+__host__ __device__ __forceinline__ int64_t fdiv64(int64_t num, int64_t den) {
+  int64_t q = static_cast<int64_t>(static_cast<double>(num) / static_cast<double>(den));
+  while (q * den > num) --q;
+  while ((q + 1) * den <= num) ++q;
+  return q;
 }
+// CTA owning tile t under the static split a0(b) = floor(b*T/grid): the largest b with a0(b) <= t
+__host__ __device__ __forceinline__ int cta_of_tile(int64_t t, int64_t T, int grid) {
+  return static_cast<int>(fdiv64((t + 1) * grid - 1, T));
+}
+
+#define KRP_TRACE(slot, idx)                                                                 \
+  do {                                                                                       \
+    if (p.trace && blockIdx.x == 0 && (idx) < 64) p.trace[(slot) * 64 + (idx)] = clock64(); \
+  } while (0)
 
 __device__ __forceinline__ uint32_t tf32_hi_bits(float x) { return __float_as_uint(x) & 0xFFFFE000u; }
 
-template <int RMAX>
+__device__ __forceinline__ float lds_f32(uint32_t saddr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(saddr));
+  return v;
+}
+__device__ __forceinline__ void sts_f32(uint32_t saddr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(saddr), "f"(v) : "memory");
+}
+
+// One 8-column epilogue round for this thread's TMEM lane: z = D[rr..rr+8) (+ D[R8+rr..] for the concat
+// form), acc += z·Ω_S; on this side's T rounds, the 32-lane transposed butterfly of z·W is written to rbuf.
+// Shared memory is addressed through 32-bit shared-window addresses: wsw[j] = swizzled byte offset of
+// (row j mod 8, this lane) inside a W row block, so every load below is base + register + immediate.
+__device__ __forceinline__ void epi_round8(int rnd, float (&acc)[8], uint32_t tD, int R, int R8, int triple,
+                                           uint32_t oms_s, bool my_t, const uint32_t (&wsw)[8],
+                                           uint32_t rbuf_s, uint32_t sub, uint32_t lane) {
+  const int rr = 8 * rnd;
+  float a[8], b[8], tv[8];
+  tmem_ld8(tD + rr, a);
+  if (!triple) tmem_ld8(tD + R8 + rr, b);
+  tmem_ld_wait();
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const bool ok = rr + j < R;
+    const float z = ok ? (triple ? a[j] : a[j] + b[j]) : 0.f;
+    acc[j] = fmaf(z, ok ? lds_f32(oms_s + (rr + j) * 4) : 0.f, acc[j]);
+    tv[j] = z;
+  }
+  if (my_t) {
+    const uint32_t lo_row = static_cast<uint32_t>(R8) * 128;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t ad = wsw[j] + (rr + j) * 128;
+      tv[j] *= lds_f32(ad) + lds_f32(ad + lo_row);
+    }
+    // 3 halving levels + 2 plain levels: lanes 4q..4q+3 end with the 32-lane sum for r = rr + q
+#pragma unroll
+    for (int lvl = 0; lvl < 3; ++lvl) {
+      const int m = 16 >> lvl;
+      const int h = 4 >> lvl;
+      const bool upper = (lane & m) != 0;
+#pragma unroll
+      for (int j = 0; j < h; ++j) {
+        const float send = upper ? tv[j] : tv[j + h];
+        const float keep = upper ? tv[j + h] : tv[j];
+        tv[j] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+      }
+    }
+    tv[0] += __shfl_xor_sync(0xffffffffu, tv[0], 2);
+    tv[0] += __shfl_xor_sync(0xffffffffu, tv[0], 1);
+    if ((lane & 3) == 0) sts_f32(rbuf_s + (sub * R8 + rr + (lane >> 2)) * 4, tv[0]);
+  }
+}
+
+// CH: TMEM A-operand chunk width (K columns per split/MMA handshake); RA: 0 = A1/A2 accumulators in
+// TMEM, else they live in registers (RA = compile-time bound on R, a multiple of 8).
+template <int CH, int RA>
 __global__ void __launch_bounds__(kThreads, 1)
     krp_tc_sketch_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ TcParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -95,7 +160,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* xs = reinterpret_cast<float*>(smem + p.sm_x);
   uint8_t* bp = smem + p.sm_bp;
   uint8_t* bq = smem + p.sm_bq;
-  float* red = reinterpret_cast<float*>(smem + p.sm_red);  // [2][4 lane quarters][RMAX]
+  float* red = reinterpret_cast<float*>(smem + p.sm_red);  // [2 parities][4 lane quarters][R8]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.sm_bar);
   uint64_t* full_x = bars;
   uint64_t* empty_x = full_x + p.NS;
@@ -105,6 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* acc_empty = acc_full + p.NA;
   uint64_t* b_ready = acc_empty + p.NA;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(b_ready + 1);
+  float* wsbuf = reinterpret_cast<float*>(smem + p.sm_ws);  // [NA][RS]: Ω_S row of the tile in acc stage a
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -112,25 +178,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < p.NS; ++i) {
       mbar_init(&full_x[i], 1);
-      mbar_init(&empty_x[i], 4);
+      mbar_init(&empty_x[i], kNumSplitWarps);
     }
     for (int i = 0; i < p.NC; ++i) {
       mbar_init(&chunk_full[i], 4);
-      mbar_init(&chunk_empty[i], 1);
+      mbar_init(&chunk_empty[i], p.do_p + p.do_q);  // one tcgen05.commit per active MMA issuer warp
     }
     for (int i = 0; i < p.NA; ++i) {
-      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_full[i], p.do_p + p.do_q + 1);  // the issuers' tcgen05.commits + the Ω_S bulk copy
       mbar_init(&acc_empty[i], kNumEpiWarps);
     }
     mbar_init(b_ready, 1);
     fence_barrier_init();
   }
-  {  // zero both B operands once: rows >= 2R stay zero (UMMA N padding)
-    float* b = reinterpret_cast<float*>(bp);
-    const int nf = 2 * p.NP * 128;
-    for (int i = threadIdx.x; i < nf; i += kThreads) b[i] = 0.f;
-  }
-  fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -138,7 +198,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * p.T / gridDim.x;
   const int64_t t1 = static_cast<int64_t>(blockIdx.x + 1) * p.T / gridDim.x;
-  const int nkc = kTile / kCH;
+  constexpr int nkc = kTile / CH;
 
   if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer
@@ -147,14 +207,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol = policy_evict_first();
       int st = 0;
       uint32_t ph = 0;
+      int64_t pair = t0 / p.S, s = t0 % p.S;
+      int rb = static_cast<int>(pair / p.CB), cb = static_cast<int>(pair % p.CB);
+      // L2 prefetch runs kPf tiles ahead of the loads (hides DRAM hiccups behind only NS SMEM stages)
+      constexpr int kPf = 3;
+      int64_t pf_t = t0, pf_pair = pair, pf_s = s;
+      auto pf_advance = [&]() {
+        if (++pf_s == p.S) {
+          pf_s = 0;
+          ++pf_pair;
+        }
+        ++pf_t;
+      };
+      for (int i = 0; i < kPf && pf_t < t1; ++i) {
+        const int prb = static_cast<int>(pf_pair / p.CB), pcb = static_cast<int>(pf_pair % p.CB);
+        for (int j = 0; j < 4; ++j) tma_prefetch_3d(&tmap, prb * kTile + 32 * j, pcb * kTile, static_cast<int32_t>(pf_s));
+        pf_advance();
+      }
       for (int64_t t = t0; t < t1; ++t) {
-        const int64_t pair = t / p.S, s = t % p.S;
-        const int rb = static_cast<int>(pair / p.CB), cb = static_cast<int>(pair % p.CB);
+        if (pf_t < t1) {
+          const int prb = static_cast<int>(pf_pair / p.CB), pcb = static_cast<int>(pf_pair % p.CB);
+          for (int j = 0; j < 4; ++j)
+            tma_prefetch_3d(&tmap, prb * kTile + 32 * j, pcb * kTile, static_cast<int32_t>(pf_s));
+          pf_advance();
+        }
         if (p.dbg == 4) {  // probe: the producer consumes its own stages (no handshake)
           if (t - t0 >= p.NS) mbar_wait(&full_x[st], ph ^ 1);
         } else {
           mbar_wait(&empty_x[st], ph ^ 1);
         }
+        KRP_TRACE(0, t - t0);
         mbar_arrive_expect_tx(&full_x[st], kStageFloats * 4);
         float* dst = xs + st * kStageFloats;
         for (int j = 0; j < 4; ++j)
@@ -164,17 +246,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           st = 0;
           ph ^= 1;
         }
+        if (++s == p.S) {
+          s = 0;
+          ++pair;
+          rb = static_cast<int>(pair / p.CB);
+          cb = static_cast<int>(pair % p.CB);
+        }
       }
       if (p.dbg == 4) {  // drain the stages still in flight
-        for (int64_t t = std::max(t0, t1 - p.NS); t < t1; ++t) {
+        for (int64_t t = (t1 - p.NS > t0 ? t1 - p.NS : t0); t < t1; ++t) {
           const int s2 = static_cast<int>((t - t0) % p.NS);
           mbar_wait(&full_x[s2], static_cast<uint32_t>(((t - t0) / p.NS) & 1));
         }
       }
     }
-  } else if (warp == kMmaWarp) {
-    // ------------------------------------------------------------ MMA issuer (one thread)
-    if (elect_one()) {
+  } else if (warp == kMmaWarp || warp == kMmaWarpQ) {
+    // ------------------------------------------------------------ MMA issuers: one thread per GEMM
+    const bool qgemm = (warp == kMmaWarpQ);
+    if (elect_one() && (qgemm ? p.do_q : p.do_p)) {
       const uint32_t idesc1 = make_idesc_tf32(128, p.NP, 0, 0);
       const uint32_t idesc2 = make_idesc_tf32(128, p.N2, 0, 0);
       const uint32_t bp_addr = smem_u32(bp), bq_addr = smem_u32(bq);
@@ -188,100 +277,142 @@ __global__ void __launch_bounds__(kThreads, 1)
           bph ^= 1;
           prev_pair = pair;
         }
-        if (p.dbg == 0) mbar_wait(&acc_empty[ast], aph ^ 1);
+        if (p.dbg == 0 || p.dbg == 5) mbar_wait(&acc_empty[ast], aph ^ 1);
+        KRP_TRACE(3, t - t0);
         tc_fence_after();
-        const uint32_t dP = tbase + p.tm_acc + ast * 2 * p.NP;
-        const uint32_t dQ = dP + p.NP;
+        if (qgemm == !p.do_p) {  // Ω_S(s, :) for the epilogue, delivered on the same barrier as the accumulator
+          const int64_t s_ = t % p.S;
+          mbar_arrive_expect_tx(&acc_full[ast], p.RS * 4);
+          bulk_copy_g2s(wsbuf + ast * p.RS, p.OmS + s_ * p.RS, p.RS * 4, &acc_full[ast]);
+        }
+        const uint32_t dP = tbase + p.tm_acc + ast * 2 * p.DN;
+        const uint32_t dQ = dP + p.DN;
         for (int kc = 0; kc < nkc; ++kc) {
           mbar_wait(&chunk_full[cst], cph);
+          KRP_TRACE(10, (t - t0) * 8 + kc);
           tc_fence_after();
-          const uint32_t ch = tbase + p.tm_chunk + cst * 4 * kCH;
+          const uint32_t ch = tbase + p.tm_chunk + cst * 4 * CH;
+          if (p.dbg != 2) {
 #pragma unroll
-          for (int ks = 0; ks < kCH / 8; ++ks) {
-            const int kk = kc * (kCH / 8) + ks;
-            const uint32_t boff = (kk >> 2) * (p.NP * 128) + (kk & 3) * 32;
-            if (p.dbg == 2) continue;
-            if (p.do_p) {
-              const uint64_t bd = make_smem_desc(bp_addr + boff, 0, 1024, kLayoutSW128);
-              mma_tf32_ts(dP, ch + 0 * kCH + 8 * ks, bd, idesc1, kk > 0 ? 1u : 0u);  // hi x [B_hi | B_lo]
-              mma_tf32_ts(dP, ch + 1 * kCH + 8 * ks, bd, idesc2, 1u);                 // lo x B_hi
-            }
-            if (p.do_q) {
-              const uint64_t bd = make_smem_desc(bq_addr + boff, 0, 1024, kLayoutSW128);
-              mma_tf32_ts(dQ, ch + 2 * kCH + 8 * ks, bd, idesc1, kk > 0 ? 1u : 0u);
-              mma_tf32_ts(dQ, ch + 3 * kCH + 8 * ks, bd, idesc2, 1u);
+            for (int ks = 0; ks < CH / 8; ++ks) {
+              const int kk = kc * (CH / 8) + ks;
+              const uint32_t boff = (kk >> 2) * (p.NP * 128) + (kk & 3) * 32;
+              const uint32_t lo_off = p.R8 * 128;  // B_lo rows start at R8 (8-row aligned)
+              if (!qgemm) {
+                const uint64_t bd = make_smem_desc(bp_addr + boff, 0, 1024, kLayoutSW128);
+                if (p.triple) {
+                  const uint64_t bl = make_smem_desc(bp_addr + boff + lo_off, 0, 1024, kLayoutSW128);
+                  mma_tf32_ts(dP, ch + 0 * CH + 8 * ks, bd, idesc2, kk > 0 ? 1u : 0u);  // hi x hi
+                  mma_tf32_ts(dP, ch + 0 * CH + 8 * ks, bl, idesc2, 1u);                 // hi x lo
+                  mma_tf32_ts(dP, ch + 1 * CH + 8 * ks, bd, idesc2, 1u);                 // lo x hi
+                } else {
+                  mma_tf32_ts(dP, ch + 0 * CH + 8 * ks, bd, idesc1, kk > 0 ? 1u : 0u);  // hi x [B_hi | B_lo]
+                  mma_tf32_ts(dP, ch + 1 * CH + 8 * ks, bd, idesc2, 1u);                 // lo x B_hi
+                }
+              }
+              if (qgemm) {
+                const uint64_t bd = make_smem_desc(bq_addr + boff, 0, 1024, kLayoutSW128);
+                if (p.triple) {
+                  const uint64_t bl = make_smem_desc(bq_addr + boff + lo_off, 0, 1024, kLayoutSW128);
+                  mma_tf32_ts(dQ, ch + 2 * CH + 8 * ks, bd, idesc2, kk > 0 ? 1u : 0u);
+                  mma_tf32_ts(dQ, ch + 2 * CH + 8 * ks, bl, idesc2, 1u);
+                  mma_tf32_ts(dQ, ch + 3 * CH + 8 * ks, bd, idesc2, 1u);
+                } else {
+                  mma_tf32_ts(dQ, ch + 2 * CH + 8 * ks, bd, idesc1, kk > 0 ? 1u : 0u);
+                  mma_tf32_ts(dQ, ch + 3 * CH + 8 * ks, bd, idesc2, 1u);
+                }
+              }
             }
           }
           mma_commit(&chunk_empty[cst]);
+          KRP_TRACE(11, (t - t0) * 8 + kc);
           if (++cst == p.NC) {
             cst = 0;
             cph ^= 1;
           }
         }
         mma_commit(&acc_full[ast]);
+        KRP_TRACE(4, t - t0);
         if (++ast == p.NA) {
           ast = 0;
           aph ^= 1;
         }
       }
     }
-  } else if (warp < 4) {
+  } else if (warp < kNumSplitWarps) {
     // ------------------------------------------------------------ split warps: SMEM tile -> TMEM hi/lo
-    const uint32_t sub = warp;  // TMEM lane quarter
+    // warp w stages the chunks kc with kc % 2 == w / 4 of every tile, for TMEM lane quarter w % 4
+    const uint32_t sub = warp & 3;
+    const int par = static_cast<int>(warp >> 2);  // chunk parity handled by this warp (kSplitPar == 2)
     const uint32_t lane_off = (32u * sub) << 16;
-    int xst = 0, cst = 0;
-    uint32_t xph = 0, cph = 0;
+    int xst = 0;
+    uint32_t xph = 0;
+    int cst = 0;  // chunk stage / phase of the chunk being processed (every chunk, both parities)
+    uint32_t cph = 0;
+    const bool dop = p.do_p && p.dbg != 5 && p.dbg != 6, doq = p.do_q && p.dbg != 5 && p.dbg != 6;
+    const int gq = static_cast<int>(32 * sub + lane);
     for (int64_t t = t0; t < t1; ++t) {
       mbar_wait(&full_x[xst], xph);
+      if (sub == 0 && par == 0 && lane == 0) KRP_TRACE(1, t - t0);
       const float* X = xs + xst * kStageFloats;
       if (p.dbg == 4) break;
       for (int kc = 0; kc < (p.dbg == 1 ? 0 : nkc); ++kc) {
-        mbar_wait(&chunk_empty[cst], cph ^ 1);
-        tc_fence_after();
-        const uint32_t ch = tbase + lane_off + p.tm_chunk + cst * 4 * kCH;
-        if (p.do_p) {
-          // lane = ρ = 32*sub + lane (box `sub`), columns γ = kc*16 + j (rows of the box)
-          const float* box = X + sub * 4096;
-          uint32_t hi[16], lo[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int g = kc * 16 + j;
-            const float x = box[g * 32 + ((((lane >> 2) ^ (g & 7))) << 2) + (lane & 3)];
-            hi[j] = __float_as_uint(x);
-            lo[j] = __float_as_uint(x - __uint_as_float(tf32_hi_bits(x)));
-          }
-          tmem_st16(ch + 0 * kCH, hi);
-          tmem_st16(ch + 1 * kCH, lo);
-        }
-        if (p.do_q) {
-          // lane = γ = 32*sub + lane, columns ρ = kc*16 + j : 16 consecutive ρ of row γ of box (kc/2)
-          const int g = 32 * sub + lane;
-          const float* row = X + (kc >> 1) * 4096 + g * 32;
-          uint32_t hi[16], lo[16];
-#pragma unroll
-          for (int qq = 0; qq < 4; ++qq) {
-            const int chunk = ((kc & 1) * 4 + qq) ^ (g & 7);
-            const float4 v = *reinterpret_cast<const float4*>(row + chunk * 4);
-            const float vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              hi[qq * 4 + e] = __float_as_uint(vv[e]);
-              lo[qq * 4 + e] = __float_as_uint(vv[e] - __uint_as_float(tf32_hi_bits(vv[e])));
-            }
-          }
-          tmem_st16(ch + 2 * kCH, hi);
-          tmem_st16(ch + 3 * kCH, lo);
-        }
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&chunk_full[cst]);
+        const int my_cst = cst;
+        const uint32_t my_cph = cph;
         if (++cst == p.NC) {
           cst = 0;
           cph ^= 1;
         }
+        if (kSplitPar == 2 && (kc & 1) != par) continue;
+        mbar_wait(&chunk_empty[my_cst], my_cph ^ 1);
+        if (sub == 0 && lane == 0) KRP_TRACE(8, (t - t0) * 8 + kc);
+        tc_fence_after();
+        const uint32_t ch = tbase + lane_off + p.tm_chunk + my_cst * 4 * CH;
+        // 16-column pieces keep the live register set small (CH may be 32)
+#pragma unroll 1
+        for (int h0 = 0; h0 < CH; h0 += 16) {
+          if (dop) {
+            // lane = ρ = 32*sub + lane (box `sub`), columns γ = kc*CH + h0 + j (rows of the box)
+            const float* box = X + sub * 4096;
+            uint32_t hi[16], lo[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int g = kc * CH + h0 + j;
+              const float x = box[g * 32 + ((((lane >> 2) ^ (g & 7))) << 2) + (lane & 3)];
+              hi[j] = __float_as_uint(x);
+              lo[j] = __float_as_uint(x - __uint_as_float(tf32_hi_bits(x)));
+            }
+            tmem_st16(ch + 0 * CH + h0, hi);
+            tmem_st16(ch + 1 * CH + h0, lo);
+          }
+          if (doq) {
+            // lane = γ = 32*sub + lane, columns ρ = kc*CH + h0 + j: 16 consecutive ρ of row γ
+            const int rho0 = kc * CH + h0;
+            const float* row = X + (rho0 >> 5) * 4096 + gq * 32;
+            uint32_t hi[16], lo[16];
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+              const int chunk = (((rho0 & 31) >> 2) + qq) ^ (gq & 7);
+              const float4 v = *reinterpret_cast<const float4*>(row + chunk * 4);
+              const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                hi[qq * 4 + e] = __float_as_uint(vv[e]);
+                lo[qq * 4 + e] = __float_as_uint(vv[e] - __uint_as_float(tf32_hi_bits(vv[e])));
+              }
+            }
+            tmem_st16(ch + 2 * CH + h0, hi);
+            tmem_st16(ch + 3 * CH + h0, lo);
+          }
+        }
+        tmem_st_wait();
+        if (sub == 0 && lane == 0) KRP_TRACE(9, (t - t0) * 8 + kc);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&chunk_full[my_cst]);
       }
       __syncwarp();
+      if (sub == 0 && par == 0 && lane == 0) KRP_TRACE(2, t - t0);
       if (lane == 0) mbar_arrive(&empty_x[xst]);
       if (++xst == p.NS) {
         xst = 0;
@@ -290,17 +421,31 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue warps
-    // warps 4-7: P side (z1 -> A1 += z1·Ω_S, T = Σ_lanes z1·W_L);  warps 8-11: Q side (A2 += z2·Ω_S)
+    // warps 8-11: P side (z1 -> A1 += z1·Ω_S), warps 12-15: Q side (z2 -> A2 += z2·Ω_S); A1/A2 live
+    // in TMEM (lane = ρ resp. γ).  T(s,r) = Σ_ρ z1·W_L = Σ_γ z2·W_R: its 8-column rounds alternate
+    // between the two sides.
     const uint32_t ew = warp - kEpiWarp0;  // 0..7
     const uint32_t sub = warp & 3;         // TMEM lane quarter
     const bool pside = ew < 4;
     const int l = static_cast<int>(32 * sub + lane);
     const uint32_t lane_off = (32u * sub) << 16;
     const uint32_t k32 = static_cast<uint32_t>(l) & 31u, katom = static_cast<uint32_t>(l) >> 5;
+    const uint32_t c0 = k32 >> 2, e0 = (k32 & 3u) * 4u;  // swizzle: byte offset in a row = ((c0 ^ (row & 7)) << 4) + e0
     const bool active = pside ? (p.do_p != 0) : (p.do_q != 0);
-    float A[RMAX];
+    const int R = p.R, R8 = p.R8;
+    const int nr = (R + 7) / 8;
+    // my side's W (B_Q = W_L rows for the P side, B_P = W_R rows for the Q side) for the T rounds
+    uint32_t wsw[8];
+    {
+      const uint32_t wb = smem_u32((pside ? bq : bp) + katom * (p.NP * 128));
 #pragma unroll
-    for (int j = 0; j < RMAX; ++j) A[j] = 0.f;
+      for (int j = 0; j < 8; ++j) wsw[j] = wb + ((c0 ^ static_cast<uint32_t>(j)) << 4) + e0;
+    }
+    const uint32_t tA = tbase + lane_off + p.tm_a + (pside ? 0 : R8);  // A1 / A2 columns
+    const uint32_t zero8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    float Areg[RA > 0 ? RA : 1];
+#pragma unroll
+    for (int j = 0; j < (RA > 0 ? RA : 1); ++j) Areg[j] = 0.f;
     int ast = 0;
     uint32_t aph = 0;
     int64_t prev_pair = -1;
@@ -311,116 +456,126 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (pair != prev_pair) {
         if (prev_pair >= 0)
         {  // flush the finished segment's accumulators into its partial slot
-          const int64_t slot = static_cast<int64_t>(blockIdx.x) * p.maxseg + seg;
+          const int64_t slot = prev_pair * p.maxseg + (blockIdx.x - cta_of_tile(prev_pair * p.S, p.T, gridDim.x));
           if (threadIdx.x == kEpiWarp0 * 32) p.slot_pair[slot] = static_cast<int>(prev_pair);
-          float* dst = (pside ? p.partA1 : p.partA2) + (slot * kTile + l) * p.R;
+          float* dst = (pside ? p.partA1 : p.partA2) + (slot * kTile + l) * R;
+          if constexpr (RA > 0) {
 #pragma unroll
-          for (int j = 0; j < RMAX; ++j) {
-            if (active && j < p.R) dst[j] = A[j];
-            A[j] = 0.f;
+            for (int j = 0; j < RA; ++j) {
+              if (active && j < R) dst[j] = Areg[j];
+              Areg[j] = 0.f;
+            }
+          } else if (active) {
+            for (int rnd = 0; rnd < nr; ++rnd) {
+              float v[8];
+              tmem_ld8(tA + 8 * rnd, v);
+              tmem_ld_wait();
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if (8 * rnd + j < R) dst[8 * rnd + j] = v[j];
+            }
           }
         }
+
         ++seg;
         prev_pair = pair;
         const int64_t rb = pair / p.CB, cb = pair % p.CB;
-        // Khatri-Rao rows of this segment -> B operands [hi | lo] (K-major, SWIZZLE_128B).
-        // P-side warps write B_Q (row lanes, W_L), Q-side warps write B_P (col lanes, W_R).
-        if (pside ? (p.do_q || p.do_t) : p.do_p) {
-          const int64_t lin = pside ? rb * kTile + l : cb * kTile + l;
-          const bool inb = lin < (pside ? p.M : p.C);
-          const float* tab = (pside ? p.WL : p.WR) + lin * p.R;
-          uint8_t* base = (pside ? bq : bp) + katom * (p.NP * 128);
-          for (int r = 0; r < p.R; ++r) {
-            const float w = inb ? __ldg(tab + r) : 0.f;
-            const float whi = __uint_as_float(tf32_hi_bits(w));
-            *reinterpret_cast<float*>(base + sw128_offset(r, k32)) = whi;
-            *reinterpret_cast<float*>(base + sw128_offset(p.R + r, k32)) = w - whi;
-          }
+        // zero this segment's accumulators (register accumulators are zeroed by the flush)
+        if (RA == 0 && active) {
+          for (int rnd = 0; rnd < nr; ++rnd) tmem_st8(tA + 8 * rnd, zero8);
+          tmem_st_wait();
+        }
+        // B operands of this segment: copy the pre-swizzled images (P side -> B_Q, Q side -> B_P)
+        {
+          const float4* src = reinterpret_cast<const float4*>(pside ? p.BQimg + rb * (p.NP * 128)
+                                                                    : p.BPimg + cb * (p.NP * 128));
+          float4* dst = reinterpret_cast<float4*>(pside ? bq : bp);
+          const int n4 = p.NP * 128 / 4;
+          const int me = static_cast<int>(sub * 32 + lane);
+#pragma unroll 4
+          for (int i = me; i < n4; i += 128) dst[i] = __ldg(src + i);
         }
         fence_proxy_async_smem();
         named_bar_sync(1, kNumEpiWarps * 32);
         if (threadIdx.x == kEpiWarp0 * 32) mbar_arrive(b_ready);
       }
-      if (p.dbg != 0) continue;
+      if (p.dbg != 0 && p.dbg != 5) continue;
       mbar_wait(&acc_full[ast], aph);
+      if (ew == 0 && lane == 0) KRP_TRACE(5, t - t0);
       tc_fence_after();
-      const uint32_t tD = tbase + lane_off + p.tm_acc + ast * 2 * p.NP + (pside ? 0 : p.NP);
-      const float* oms = p.OmS + s * p.R;
-      const uint8_t* wlbase = bq + katom * (p.NP * 128);
-      float* rbuf = red + parity * (4 * RMAX);
-      const bool dot = pside && p.do_t;
+      const uint32_t tD = tbase + lane_off + p.tm_acc + ast * 2 * p.DN + (pside ? 0 : p.DN);
+      const uint32_t oms_s = smem_u32(wsbuf + ast * p.RS);
+      const uint32_t rbuf_s = smem_u32(red + parity * (4 * R8));
+      float* rbuf = red + parity * (4 * R8);
+      if (active) {
+        if constexpr (RA > 0) {
 #pragma unroll
-      for (int rnd = 0; rnd < RMAX / 16; ++rnd) {
-        const int rr = 16 * rnd;
-        float tv[16];
-        if (active) {
-          float a[16], b[16];
-          tmem_ld16(tD + rr, a);
-          tmem_ld16(tD + p.R + rr, b);
-          tmem_ld_wait();
+          for (int rnd = 0; rnd < RA / 8; ++rnd) {
+            if (8 * rnd < R) {
+              float acc8[8];  // register copies (no pointer into Areg, which must stay in registers)
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int r = rr + j;
-            float z = 0.f, ws = 0.f, wl = 0.f;
-            if (r < p.R) {
-              z = a[j] + b[j];
-              ws = __ldg(oms + r);
-              if (dot)
-                wl = *reinterpret_cast<const float*>(wlbase + sw128_offset(r, k32)) +
-                     *reinterpret_cast<const float*>(wlbase + sw128_offset(p.R + r, k32));
-            }
-            A[rr + j] = fmaf(z, ws, A[rr + j]);
-            tv[j] = z * wl;
-          }
-        }
-        if (rnd == RMAX / 16 - 1) {
-          // every TMEM read of this tile is done: hand the accumulator stage back to the MMA warp
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&acc_empty[ast]);
-        }
-        if (dot) {
-          // transposed butterfly over the 32 lanes: lanes 2q, 2q+1 end with the sum for r = rr + q
+              for (int j = 0; j < 8; ++j) acc8[j] = Areg[8 * rnd + j];
+              epi_round8(rnd, acc8, tD, R, R8, p.triple, oms_s, p.do_t && ((rnd & 1) == (pside ? 0 : 1)), wsw, rbuf_s, sub,
+                         lane);
 #pragma unroll
-          for (int lvl = 0; lvl < 4; ++lvl) {
-            const int m = 16 >> lvl;
-            const int h = 8 >> lvl;
-            const bool upper = (lane & m) != 0;
-#pragma unroll
-            for (int j = 0; j < h; ++j) {
-              const float send = upper ? tv[j] : tv[j + h];
-              const float keep = upper ? tv[j + h] : tv[j];
-              tv[j] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+              for (int j = 0; j < 8; ++j) Areg[8 * rnd + j] = acc8[j];
             }
           }
-          tv[0] += __shfl_xor_sync(0xffffffffu, tv[0], 1);
-          if ((lane & 1) == 0) rbuf[sub * RMAX + rr + (lane >> 1)] = tv[0];
+        } else {
+          for (int rnd = 0; rnd < nr; ++rnd) {
+            float acc[8];
+            tmem_ld8(tA + 8 * rnd, acc);
+            epi_round8(rnd, acc, tD, R, R8, p.triple, oms_s, p.do_t && ((rnd & 1) == (pside ? 0 : 1)), wsw, rbuf_s, sub,
+                       lane);
+            uint32_t accb[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) accb[j] = __float_as_uint(acc[j]);
+            tmem_st8(tA + 8 * rnd, accb);
+          }
+          tmem_st_wait();
         }
       }
+      // every TMEM read of this tile is done: hand the accumulator stage back to the MMA warp
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[ast]);
       if (++ast == p.NA) {
         ast = 0;
         aph ^= 1;
       }
-      if (dot) {
-        // fixed-order sum of the four lane quarters (P-side warps only)
-        named_bar_sync(2, 4 * 32);
-        const int e = static_cast<int>(sub * 32 + lane);
-        if (e < p.R) {
-          const float tot = ((rbuf[e] + rbuf[RMAX + e]) + rbuf[2 * RMAX + e]) + rbuf[3 * RMAX + e];
-          p.Tpart[(pair * p.S + s) * p.R + e] = tot;
+      if (p.do_t) {
+        // fixed-order sum of the four lane quarters for every r (the two sides wrote disjoint rounds)
+        named_bar_sync(2, kNumEpiWarps * 32);
+        const int e = static_cast<int>(ew * 32 + lane);
+        if (e < R) {
+          const float tot = ((rbuf[e] + rbuf[R8 + e]) + rbuf[2 * R8 + e]) + rbuf[3 * R8 + e];
+          p.Tpart[(pair * p.S + s) * R + e] = tot;
         }
         parity ^= 1;
       }
+      if (ew == 0 && lane == 0) KRP_TRACE(6, t - t0);
+      if (ew == 4 && lane == 0) KRP_TRACE(7, t - t0);
     }
     if (prev_pair >= 0)
         {  // flush the finished segment's accumulators into its partial slot
-          const int64_t slot = static_cast<int64_t>(blockIdx.x) * p.maxseg + seg;
+          const int64_t slot = prev_pair * p.maxseg + (blockIdx.x - cta_of_tile(prev_pair * p.S, p.T, gridDim.x));
           if (threadIdx.x == kEpiWarp0 * 32) p.slot_pair[slot] = static_cast<int>(prev_pair);
-          float* dst = (pside ? p.partA1 : p.partA2) + (slot * kTile + l) * p.R;
+          float* dst = (pside ? p.partA1 : p.partA2) + (slot * kTile + l) * R;
+          if constexpr (RA > 0) {
 #pragma unroll
-          for (int j = 0; j < RMAX; ++j) {
-            if (active && j < p.R) dst[j] = A[j];
-            A[j] = 0.f;
+            for (int j = 0; j < RA; ++j) {
+              if (active && j < R) dst[j] = Areg[j];
+              Areg[j] = 0.f;
+            }
+          } else if (active) {
+            for (int rnd = 0; rnd < nr; ++rnd) {
+              float v[8];
+              tmem_ld8(tA + 8 * rnd, v);
+              tmem_ld_wait();
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if (8 * rnd + j < R) dst[8 * rnd + j] = v[j];
+            }
           }
         }
   }
@@ -432,37 +587,61 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ------------------------------------------------------------------ Khatri-Rao tables
 struct TabParams {
-  int d, m, m2, R;
+  int d, m, m2, R, RS, R8, NP, RB, CB;
   int64_t M, C, S;
   int64_t n[kMaxD];
   int64_t gs[kMaxD];
   const float* om[kMaxD];
-  float *WL, *WR, *OmS;
+  float *BPimg, *BQimg, *OmS;
 };
 
-// WL(ρ,r) = Π_{k<m} Ω_k(i_k(ρ),r), WR(γ,r) = Π_{m<=k<m2} Ω_k(..), OmS(s,r) = Π_{k>=m2} Ω_k(..)
+// B-operand images in the exact shared-memory layout the UMMA descriptors expect (K-major,
+// SWIZZLE_128B, [k-atom][NP rows][128 B]): row n < R holds hi(W(lane, n)), row R8 + n holds
+// lo = W - hi, other rows are zero.  W_L(ρ,r) = Π_{k<m} Ω_k(i_k(ρ),r) for the row blocks (BQimg),
+// W_R(γ,r) = Π_{m<=k<m2} Ω_k(i_k(γ),r) for the col blocks (BPimg).  OmS(s,r) = Π_{k>=m2} Ω_k(i_k(s),r).
 __global__ void tc_tables_kernel(const __grid_constant__ TabParams p) {
   int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t nl = p.M * p.R, nr = p.C * p.R, ns = p.S * p.R;
-  int k0, k1;
-  float* out;
-  if (idx < nl) {
-    k0 = 0, k1 = p.m, out = p.WL;
-  } else if ((idx -= nl) < nr) {
-    k0 = p.m, k1 = p.m2, out = p.WR;
-  } else if ((idx -= nr) < ns) {
-    k0 = p.m2, k1 = p.d, out = p.OmS;
-  } else {
-    return;
+  const int64_t per_blk = static_cast<int64_t>(p.NP) * kTile;
+  const int64_t nq = p.RB * per_blk, np_ = p.CB * per_blk, ns = p.S * p.RS;
+  if (idx < nq + np_) {
+    const bool rows = idx < nq;
+    if (!rows) idx -= nq;
+    const int64_t blk = idx / per_blk;
+    const int rem = static_cast<int>(idx - blk * per_blk);
+    // rem enumerates (n, l) with l fastest
+    const int n = rem / kTile, l = rem % kTile;
+    const int64_t lin = blk * kTile + l;
+    float v = 0.f;
+    const int r = n < p.R ? n : (n >= p.R8 && n < p.R8 + p.R ? n - p.R8 : -1);
+    if (r >= 0 && lin < (rows ? p.M : p.C)) {
+      float w = 1.f;
+      for (int k = rows ? 0 : p.m; k < (rows ? p.m : p.m2); ++k) {
+        if (!p.om[k]) continue;  // Ω_n of a single-mode sketch is not given: it never reaches Y_n
+        const int64_t ik = (lin / p.gs[k]) % p.n[k];
+        w *= __ldg(p.om[k] + ik * p.R + r);
+      }
+      const float whi = __uint_as_float(tf32_hi_bits(w));
+      v = (n < p.R) ? whi : w - whi;
+    }
+    const uint32_t k32 = static_cast<uint32_t>(l) & 31u;
+    const size_t off = static_cast<size_t>(l >> 5) * (p.NP * 128) + static_cast<size_t>(n) * 128 +
+                       (((k32 >> 2) ^ (static_cast<uint32_t>(n) & 7u)) << 4) + (k32 & 3u) * 4u;
+    float* img = (rows ? p.BQimg : p.BPimg) + blk * per_blk;
+    *reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(img) + off) = v;
+  } else if ((idx -= nq + np_) < ns) {
+    const int64_t sl = idx / p.RS;
+    const int r = static_cast<int>(idx - sl * p.RS);
+    float w = 0.f;
+    if (r < p.R) {
+      w = 1.f;
+      for (int k = p.m2; k < p.d; ++k) {
+        if (!p.om[k]) continue;
+        const int64_t ik = (sl / p.gs[k]) % p.n[k];
+        w *= __ldg(p.om[k] + ik * p.R + r);
+      }
+    }
+    p.OmS[idx] = w;
   }
-  const int64_t lin = idx / p.R;
-  const int r = static_cast<int>(idx - lin * p.R);
-  float w = 1.f;
-  for (int k = k0; k < k1; ++k) {
-    const int64_t ik = (lin / p.gs[k]) % p.n[k];
-    w *= __ldg(p.om[k] + ik * p.R + r);
-  }
-  out[idx] = w;
 }
 
 // ------------------------------------------------------------------ reduction of partials + multi-TTVs
@@ -473,11 +652,6 @@ struct RedParams {
   const float *partA1, *partA2, *Tpart;
   float *Pm, *Qc, *Ts;
 };
-
-// CTA owning tile t under the static split a0(b) = floor(b*T/grid)
-__device__ __forceinline__ int cta_of(int64_t t, int64_t T, int grid) {
-  return static_cast<int>(((t + 1) * grid - 1) / T);
-}
 
 // P(ρ,r) = Σ_{cb} Σ_{CTAs b of pair (rb,cb)} partA1[slot(b,pair)][ρ%128][r]   (fixed order)
 // Qc(γ,r) likewise over rb;  Ts(s,r) = Σ_{pairs} Tpart[pair][s][r]
@@ -495,12 +669,9 @@ __global__ void tc_assemble_kernel(const __grid_constant__ RedParams p) {
     float acc = 0.f;
     for (int o = 0; o < nother; ++o) {
       const int64_t pair = rows ? (static_cast<int64_t>(blk) * p.CB + o) : (static_cast<int64_t>(o) * p.CB + blk);
-      const int b0 = cta_of(pair * p.S, p.T, p.grid), b1 = cta_of((pair + 1) * p.S - 1, p.T, p.grid);
-      for (int b = b0; b <= b1; ++b) {
-        const int64_t a0 = static_cast<int64_t>(b) * p.T / p.grid;
-        const int64_t slot = static_cast<int64_t>(b) * p.maxseg + (pair - a0 / p.S);
-        acc += part[(slot * kTile + l) * p.R + r];
-      }
+      const int nk = cta_of_tile((pair + 1) * p.S - 1, p.T, p.grid) - cta_of_tile(pair * p.S, p.T, p.grid) + 1;
+      const float* src = part + ((pair * p.maxseg) * kTile + l) * p.R + r;
+      for (int k = 0; k < nk; ++k) acc += src[static_cast<int64_t>(k) * kTile * p.R];
     }
     (rows ? p.Pm : p.Qc)[idx] = acc;
   } else if ((idx -= nP + nQ) < nT) {
@@ -572,11 +743,11 @@ struct TcPlan {
   int64_t M = 0, C = 0, S = 0;
   int RB = 0, CB = 0;
   int64_t T = 0;
-  int R = 0, NP = 0, N2 = 0, NS = 0, NC = 0, NA = 0;
+  int R = 0, NP = 0, N2 = 0, R8 = 0, RS = 0, NS = 0, NC = 0, NA = 0, CH = 16, triple = 0, DN = 0, RA = 0;
   int do_p = 0, do_q = 0, do_t = 0;
   int grid = 0, maxseg = 0, nslot = 0;
-  int tm_acc = 0, tm_chunk = 0;
-  uint32_t sm_x = 0, sm_bp = 0, sm_bq = 0, sm_red = 0, sm_bar = 0, smem_bytes = 0;
+  int tm_acc = 0, tm_chunk = 0, tm_a = 0;
+  uint32_t sm_x = 0, sm_bp = 0, sm_bq = 0, sm_red = 0, sm_bar = 0, sm_ws = 0, smem_bytes = 0;
 };
 
 int num_sms() {
@@ -632,19 +803,43 @@ bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, TcPlan& pl
   pl.T = static_cast<int64_t>(pl.RB) * pl.CB * S;
   pl.R = R;
   pl.do_t = ws ? 1 : 0;
-  pl.do_p = (wr || ws) ? 1 : 0;  // T is computed from z1
-  pl.do_q = wc ? 1 : 0;
-  pl.NP = round16(2 * R);
+  pl.do_p = (wr || ws) ? 1 : 0;  // T rounds alternate between z1 (P side) and z2 (Q side)
+  pl.do_q = (wc || ws) ? 1 : 0;
+  pl.R8 = (R + 7) / 8 * 8;
+  pl.RS = (R + 3) / 4 * 4;
   pl.N2 = round16(R);
-  // TMEM: NA accumulator stages of 2*NP columns, NC chunk stages of 4*kCH columns, 512 total
-  pl.NA = (4 * pl.NP + 2 * 4 * kCH <= 512) ? 2 : 1;
-  pl.NC = std::min(4, (512 - pl.NA * 2 * pl.NP) / (4 * kCH));
-  if (pl.NC < 2) return false;
+  // TMEM (512 columns): NA accumulator stages of 2*DN, NC A-chunk stages of 4*CH, and A1 + A2 (2*R8) when
+  // they do not live in registers.  The [hi|lo] concat form is 2 MMAs per K-step (DN = round16(R8 + R)),
+  // the triple form 3 MMAs of N = N2 (DN = N2).  Large chunks amortise the split -> MMA handshake.
+  {
+    struct Opt {
+      int triple, na, ch, ncmin, areg;
+    } opts[5] = {{0, 2, 32, 2, 1}, {1, 2, 32, 2, 1}, {0, 2, 16, 3, 0}, {1, 2, 16, 2, 0}, {1, 1, 16, 2, 0}};
+    pl.NC = 0;
+    for (const Opt& o : opts) {
+      if (o.areg && pl.R8 > 48) continue;  // register accumulators up to R = 48
+      const int dn = o.triple ? pl.N2 : round16(pl.R8 + R);
+      const int acols = o.areg ? 0 : 2 * pl.R8;
+      const int nc = std::min(4, (512 - o.na * 2 * dn - acols) / (4 * o.ch));
+      if (nc >= o.ncmin) {
+        pl.triple = o.triple;
+        pl.DN = dn;
+        pl.NA = o.na;
+        pl.CH = o.ch;
+        pl.NC = nc;
+        pl.RA = o.areg ? (pl.R8 <= 16 ? 16 : (pl.R8 <= 32 ? 32 : 48)) : 0;
+        break;
+      }
+    }
+    if (pl.NC < 2) return false;
+    pl.NP = pl.triple ? pl.R8 + pl.N2 : pl.DN;  // B-image rows (hi rows [0,R), lo rows [R8, R8+R))
+  }
   pl.tm_acc = 0;
-  pl.tm_chunk = pl.NA * 2 * pl.NP;
+  pl.tm_chunk = pl.NA * 2 * pl.DN;
+  pl.tm_a = pl.tm_chunk + pl.NC * 4 * pl.CH;
   // SMEM: X stages (64 KB each), B_P and B_Q (NP rows x 512 B each), reduction scratch, barriers
   const uint32_t bbytes = static_cast<uint32_t>(pl.NP) * 512u;
-  const uint32_t misc = 2 * kNumEpiWarps * 32 * 4 + 512;
+  const uint32_t misc = 2 * 4 * kMaxTcR * 4 + 256 + 2 * kMaxTcR * 4;
   const uint32_t budget = 232448 - 1024;
   int ns = static_cast<int>((budget - 2 * bbytes - misc) / (kStageFloats * 4));
   if (ns < 1) return false;
@@ -653,19 +848,17 @@ bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, TcPlan& pl
   pl.sm_bp = pl.NS * kStageFloats * 4;
   pl.sm_bq = pl.sm_bp + bbytes;
   pl.sm_red = pl.sm_bq + bbytes;
-  pl.sm_bar = pl.sm_red + 2 * kNumEpiWarps * 32 * 4;
-  pl.smem_bytes = pl.sm_bar + 512 + 1024;
+  pl.sm_bar = pl.sm_red + 2 * 4 * kMaxTcR * 4;
+  pl.sm_ws = pl.sm_bar + 256;
+  pl.smem_bytes = pl.sm_ws + 2 * kMaxTcR * 4 + 1024;
   pl.grid = static_cast<int>(std::min<int64_t>(num_sms(), pl.T));
-  // segments per CTA (distinct (rb, cb) pairs in its contiguous tile range)
-  int mx = 0;
-  for (int b = 0; b < pl.grid; ++b) {
-    const int64_t a0 = static_cast<int64_t>(b) * pl.T / pl.grid, a1 = static_cast<int64_t>(b + 1) * pl.T / pl.grid;
-    if (a1 <= a0) continue;
-    const int segs = static_cast<int>((a1 - 1) / S - a0 / S + 1);
-    mx = std::max(mx, segs);
+  // CTAs per (rb, cb) pair: a pair's S consecutive tiles meet at most ceil(S / floor(T/grid)) + 1
+  // consecutive CTAs of the static split (each CTA owns >= floor(T/grid) consecutive tiles)
+  {
+    const int64_t per_cta = std::max<int64_t>(1, pl.T / pl.grid);
+    pl.maxseg = static_cast<int>((S + per_cta - 1) / per_cta + 1);
+    pl.nslot = static_cast<int>(static_cast<int64_t>(pl.RB) * pl.CB * pl.maxseg);
   }
-  pl.maxseg = std::max(mx, 1);
-  pl.nslot = pl.grid * pl.maxseg;
   pl.ok = true;
   return true;
 }
@@ -708,6 +901,8 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
+long long* g_trace_dev = nullptr;
+
 struct WsLayout {
   size_t a1, a2, slots, tpart, pm, qc, ts, wl, wr, oms, total;
 };
@@ -727,9 +922,9 @@ WsLayout ws_layout(const TcPlan& pl) {
   w.pm = take(static_cast<size_t>(pl.M) * pl.R * sizeof(float));
   w.qc = take(static_cast<size_t>(pl.C) * pl.R * sizeof(float));
   w.ts = take(static_cast<size_t>(pl.S) * pl.R * sizeof(float));
-  w.wl = take(static_cast<size_t>(pl.M) * pl.R * sizeof(float));
-  w.wr = take(static_cast<size_t>(pl.C) * pl.R * sizeof(float));
-  w.oms = take(static_cast<size_t>(pl.S) * pl.R * sizeof(float));
+  w.wl = take(static_cast<size_t>(pl.RB) * pl.NP * kTile * sizeof(float));  // B_Q images
+  w.wr = take(static_cast<size_t>(pl.CB) * pl.NP * kTile * sizeof(float));  // B_P images
+  w.oms = take(static_cast<size_t>(pl.S) * pl.RS * sizeof(float));
   w.total = off;
   return w;
 }
@@ -777,6 +972,10 @@ int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const b
   p.R = R;
   p.NP = pl.NP;
   p.N2 = pl.N2;
+  p.R8 = pl.R8;
+  p.RS = pl.RS;
+  p.triple = pl.triple;
+  p.DN = pl.DN;
   p.NS = pl.NS;
   p.NC = pl.NC;
   p.NA = pl.NA;
@@ -786,25 +985,21 @@ int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const b
   p.maxseg = pl.maxseg;
   p.tm_acc = pl.tm_acc;
   p.tm_chunk = pl.tm_chunk;
+  p.tm_a = pl.tm_a;
   p.sm_x = pl.sm_x;
   p.sm_bp = pl.sm_bp;
   p.sm_bq = pl.sm_bq;
   p.sm_red = pl.sm_red;
   p.sm_bar = pl.sm_bar;
-  p.m = pl.m;
-  p.m2 = pl.m2;
-  p.d = g.d;
-  for (int k = 0; k < g.d; ++k) {
-    p.n[k] = g.n[k];
-    p.om[k] = om.p[k];
-  }
-  {  // strides inside each group
+  p.sm_ws = pl.sm_ws;
+  int64_t gs[kMaxD];  // stride of mode k inside its group (rows / cols / slices)
+  {
     int64_t st = 1;
-    for (int k = 0; k < pl.m; ++k) p.gs[k] = st, st *= g.n[k];
+    for (int k = 0; k < pl.m; ++k) gs[k] = st, st *= g.n[k];
     st = 1;
-    for (int k = pl.m; k < pl.m2; ++k) p.gs[k] = st, st *= g.n[k];
+    for (int k = pl.m; k < pl.m2; ++k) gs[k] = st, st *= g.n[k];
     st = 1;
-    for (int k = pl.m2; k < g.d; ++k) p.gs[k] = st, st *= g.n[k];
+    for (int k = pl.m2; k < g.d; ++k) gs[k] = st, st *= g.n[k];
   }
   p.partA1 = reinterpret_cast<float*>(wsb + wl.a1);
   p.partA2 = reinterpret_cast<float*>(wsb + wl.a2);
@@ -813,15 +1008,22 @@ int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const b
   float* Pm = reinterpret_cast<float*>(wsb + wl.pm);
   float* Qc = reinterpret_cast<float*>(wsb + wl.qc);
   float* Ts = reinterpret_cast<float*>(wsb + wl.ts);
-  float* WL = reinterpret_cast<float*>(wsb + wl.wl);
-  float* WR = reinterpret_cast<float*>(wsb + wl.wr);
+  float* BQimg = reinterpret_cast<float*>(wsb + wl.wl);
+  float* BPimg = reinterpret_cast<float*>(wsb + wl.wr);
   float* OmS = reinterpret_cast<float*>(wsb + wl.oms);
-  p.WL = WL;
-  p.WR = WR;
+  p.BQimg = BQimg;
+  p.BPimg = BPimg;
   p.OmS = OmS;
   {
     const char* e = getenv("KRP_TC_DEBUG");
     p.dbg = e ? atoi(e) : 0;
+    p.trace = nullptr;
+    if (getenv("KRP_TC_TRACE")) {
+      static long long* tr = nullptr;
+      if (!tr) cudaMalloc(&tr, 16 * 64 * sizeof(long long));
+      cudaMemsetAsync(tr, 0, 16 * 64 * sizeof(long long), s);
+      p.trace = tr;
+    }
   }
 
   CUtensorMap tmap;
@@ -839,39 +1041,53 @@ int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const b
       return KRP_ECUDA;
     }
   }
-  // 1. Khatri-Rao tables of the three mode groups (tiny: (M + C + S) x R)
+  // 1. Khatri-Rao tables: B-operand images of every row / col block, and the slice-mode rows
   {
     TabParams tp{};
     tp.d = g.d;
     tp.m = pl.m;
     tp.m2 = pl.m2;
     tp.R = R;
+    tp.RS = pl.RS;
+    tp.R8 = pl.R8;
+    tp.NP = pl.NP;
+    tp.RB = pl.RB;
+    tp.CB = pl.CB;
     tp.M = pl.M;
     tp.C = pl.C;
     tp.S = pl.S;
     for (int k = 0; k < g.d; ++k) {
-      tp.n[k] = p.n[k];
-      tp.gs[k] = p.gs[k];
-      tp.om[k] = p.om[k];
+      tp.n[k] = g.n[k];
+      tp.gs[k] = gs[k];
+      tp.om[k] = om.p[k];
     }
-    tp.WL = WL;
-    tp.WR = WR;
+    tp.BPimg = BPimg;
+    tp.BQimg = BQimg;
     tp.OmS = OmS;
-    const int64_t nt = (pl.M + pl.C + pl.S) * R;
+    const int64_t nt = (static_cast<int64_t>(pl.RB) + pl.CB) * pl.NP * kTile + pl.S * pl.RS;
     tc_tables_kernel<<<static_cast<unsigned>((nt + 255) / 256), 256, 0, s>>>(tp);
     KRP_CHECK_LAUNCH();
   }
   // 2. the fused tile kernel
-  auto kern = (R <= 16)   ? krp_tc_sketch_kernel<16>
-              : (R <= 32) ? krp_tc_sketch_kernel<32>
-              : (R <= 48) ? krp_tc_sketch_kernel<48>
-                          : krp_tc_sketch_kernel<64>;
+  auto kern = (pl.CH == 32)   ? (pl.RA == 16 ? krp_tc_sketch_kernel<32, 16>
+                                 : pl.RA == 32 ? krp_tc_sketch_kernel<32, 32>
+                                               : krp_tc_sketch_kernel<32, 48>)
+                              : krp_tc_sketch_kernel<16, 0>;
   KRP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(pl.smem_bytes)));
   prof_begin(s);
   kern<<<pl.grid, kThreads, pl.smem_bytes, s>>>(tmap, p);
   KRP_CHECK_LAUNCH();
   prof_end(s, 4.0 * static_cast<double>(g.N), 2.0 * static_cast<double>(g.N) * R * (pl.do_p + pl.do_q));
+  if (p.trace) {  // development: dump CTA 0's role timeline (KRP_TC_TRACE=<file>)
+    long long h[16 * 64];
+    cudaMemcpyAsync(h, p.trace, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    if (FILE* f = fopen(getenv("KRP_TC_TRACE"), "w")) {
+      for (int i = 0; i < 16 * 64; ++i) fprintf(f, "%lld%c", h[i], (i % 64 == 63) ? '\n' : ' ');
+      fclose(f);
+    }
+  }
   // 3. fixed-order sum of the per-CTA partials, then the multi-TTVs of the three groups
   {
     RedParams rp{};
@@ -908,9 +1124,9 @@ int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const b
     tv.S = pl.S;
     int64_t nout = 0;
     for (int k = 0; k < g.d; ++k) {
-      tv.n[k] = p.n[k];
-      tv.gs[k] = p.gs[k];
-      tv.om[k] = p.om[k];
+      tv.n[k] = g.n[k];
+      tv.gs[k] = gs[k];
+      tv.om[k] = om.p[k];
       tv.want[k] = want[k] ? 1 : 0;
       tv.y[k] = want[k] ? Y[k] : nullptr;
       if (want[k]) nout += g.n[k] * R;

@@ -199,6 +199,20 @@ __global__ void __launch_bounds__(256, 1) tp_kernel(int iters, unsigned long lon
           } else if (MODE == 3) {
             const uint32_t id80 = make_idesc_tf32(128, 80, 0, 0);
             mma_tf32_ts(d, tbase + 256 + (kk & 15) * 8, b, (kk & 1) ? idesc : id80, kk > 0);
+          } else if (MODE == 6 || MODE == 7 || MODE == 8) {
+            // kernel-like: per K-step 3 MMAs (hi.hi, hi.lo with B at +5120 B, lo.hi), two GEMMs (D at 0 / 48)
+            // MODE 6: A at 256.., D at slot*128 (+0/+48) ; MODE 7: kernel TMEM layout (A at 192.., D at slot*96)
+            // MODE 8: MODE 7 but only one GEMM (D at slot*96)
+            const uint32_t abase = (MODE == 6) ? 256u : 192u;
+            const uint32_t dslot = (MODE == 6) ? slot * 128 : slot * 96;
+            const uint32_t acol = abase + (kk & 1) * 64 + ((kk >> 1) & 1) * 8;
+            uint64_t bl = make_smem_desc(bb + (kk >> 2) * (N * 128) + (kk & 3) * 32 + 5120, 0, 1024, kLayoutSW128);
+            for (int g = 0; g < (MODE == 8 ? 1 : 2); ++g) {
+              const uint32_t dd = tbase + dslot + g * 48;
+              mma_tf32_ts(dd, tbase + acol + g * 32, b, idesc, kk > 0);
+              mma_tf32_ts(dd, tbase + acol + g * 32, bl, idesc, 1);
+              mma_tf32_ts(dd, tbase + acol + g * 32 + 16, b, idesc, 1);
+            }
           } else if (MODE == 4) {
             uint64_t a = make_smem_desc(ab + (kk >> 2) * 16384 + (kk & 3) * 32, 0, 1024, kLayoutSW128);
             const uint32_t idf = (1u << 4) | (0u << 7) | (0u << 10) | ((N >> 3) << 17) | ((128 >> 4) << 24);
@@ -293,6 +307,75 @@ void run_tmem_bw(int nsm) {
   printf("TMEM ld (4 warps, x16 + wait each): %.1f B/cyc/SM ; TMEM st x16: %.1f B/cyc/SM\n", bytes / c[0], bytes / c[1]);
 }
 
+// Chunked issue like the sketch kernel: per chunk 12 MMAs (2 K-steps x 2 GEMMs x 3), then commit to
+// chunk_empty[c]; before a chunk, wait (on chunk_empty of the chunk NC earlier) + fence.
+template <int NC, int WAITMODE>
+__global__ void __launch_bounds__(256, 1) chunk_kernel(int iters, unsigned long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  TpSmem& s = *reinterpret_cast<TpSmem*>(smem_raw);
+  __shared__ uint64_t cb[8];
+  const uint32_t tid = threadIdx.x, warp = tid >> 5;
+  if (warp == 0) tmem_alloc<512>(&s.tmem_base);
+  if (tid == 0) {
+    for (int i = 0; i < 8; ++i) mbar_init(&cb[i], 1);
+    fence_barrier_init();
+  }
+  for (int i = tid; i < 4 * 128 * 32; i += 256) (&s.b[0][0][0])[i] = 1.0f;
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = s.tmem_base;
+  if (warp == 0 && elect_one()) {
+    const uint32_t bb = smem_u32(&s.b[0][0][0]);
+    const uint32_t idesc = make_idesc_tf32(128, 48, 0, 0);
+    long long t0 = clock64();
+    int nchunks = iters * 8;
+    for (int c = 0; c < nchunks; ++c) {
+      const int st = c % NC;
+      if (WAITMODE == 1 && c >= NC) mbar_wait(&cb[st], ((c / NC) - 1) & 1);
+      tc_fence_after();
+      for (int ks = 0; ks < 2; ++ks) {
+        const int kk = (c * 2 + ks) & 15;
+        uint64_t b = make_smem_desc(bb + (kk >> 2) * (48 * 128) + (kk & 3) * 32, 0, 1024, kLayoutSW128);
+        uint64_t bl = make_smem_desc(bb + (kk >> 2) * (48 * 128) + (kk & 3) * 32 + 5120, 0, 1024, kLayoutSW128);
+        const uint32_t acol = 192 + st * 64 + ks * 8;
+        for (int g = 0; g < 2; ++g) {
+          const uint32_t dd = tbase + ((c / 8) & 1) * 96 + g * 48;
+          mma_tf32_ts(dd, tbase + acol + g * 32, b, idesc, kk > 0);
+          mma_tf32_ts(dd, tbase + acol + g * 32, bl, idesc, 1);
+          mma_tf32_ts(dd, tbase + acol + g * 32 + 16, b, idesc, 1);
+        }
+      }
+      mma_commit(&cb[st]);
+    }
+    for (int c = nchunks - NC; c < nchunks; ++c) mbar_wait(&cb[c % NC], (c / NC) & 1);
+    long long t1 = clock64();
+    cycles[blockIdx.x] = (unsigned long long)(t1 - t0);
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tbase);
+}
+
+template <int NC, int WAITMODE>
+void run_chunk(const char* name, int nsm) {
+  auto k = chunk_kernel<NC, WAITMODE>;
+  size_t smem = sizeof(TpSmem) + 1024;
+  CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  unsigned long long* dcyc;
+  CK(cudaMalloc(&dcyc, nsm * sizeof(unsigned long long)));
+  k<<<nsm, 256, smem>>>(10, dcyc);
+  CK(cudaDeviceSynchronize());
+  k<<<nsm, 256, smem>>>(500, dcyc);
+  CK(cudaDeviceSynchronize());
+  unsigned long long c;
+  CK(cudaMemcpy(&c, dcyc, 8, cudaMemcpyDeviceToHost));
+  printf("%-40s NC=%d: %.1f cyc/chunk (12 MMAs), %.1f cyc/mma\n", name, NC, c / 4000.0, c / 48000.0);
+  cudaFree(dcyc);
+}
+
 template <int MODE, int N, int HAMMER>
 void run_tp(const char* name, int nsm) {
   auto k = tp_kernel<MODE, N, HAMMER>;
@@ -324,7 +407,7 @@ void run_tp(const char* name, int nsm) {
     const double bytes = (double)(iters * 16 * N / 64) * 16 * 16 * 128;
     printf("   hammer: %.1f B/cyc/SM LDS over %.0f cyc (mma region %.0f cyc)\n", bytes / hx, hx, mx);
   }
-  const double n_mma = (double)iters * 16;
+  const double n_mma = (double)iters * 16 * ((MODE == 6 || MODE == 7) ? 6 : (MODE == 8 ? 3 : 1));
   const double flops = 2.0 * 128 * N * ((MODE >= 4) ? 16 : 8) * n_mma * nsm;
   printf("%-28s N=%3d hammer=%d  cyc/mma=%7.2f  (floor %5.1f)  TF32 TFLOP/s=%7.1f  clk=%.0f MHz\n", name, N,
          HAMMER, mx / n_mma, 128.0 * N / 256.0, flops / (ms * 1e-3) / 1e12, mx / (ms * 1e-3) / 1e6);
@@ -424,6 +507,15 @@ int main() {
   }
   // ---------------- throughput
   const int nsm = prop.multiProcessorCount;
+  run_chunk<3, 0>("chunked, commits, no waits", nsm);
+  run_chunk<3, 1>("chunked, commit + wait NC back", nsm);
+  run_chunk<2, 1>("chunked, commit + wait NC back", nsm);
+  run_chunk<6, 1>("chunked, commit + wait NC back", nsm);
+  run_tp<2, 48, 0>("TS single", nsm);
+  run_tp<6, 48, 0>("TS kernel-mix (A@256)", nsm);
+  run_tp<7, 48, 0>("TS kernel-mix (kernel TMEM)", nsm);
+  run_tp<8, 48, 0>("TS kernel-mix 1 GEMM", nsm);
+  return 0;
   run_tp<0, 80, 0>("SS Kmaj", nsm);
   run_tp<0, 128, 0>("SS Kmaj", nsm);
   run_tp<2, 16, 0>("TS", nsm);
