@@ -91,6 +91,9 @@ class ClockSampler:
             pynvml.nvmlInit()
             self.th = threading.Thread(target=self._poll, daemon=True)
             self.th.start()
+            t0 = time.time()
+            while not self.samples and time.time() - t0 < 1.0:  # the timed region starts once sampling runs
+                time.sleep(0.001)
         except Exception:
             self.th = None
 
@@ -371,8 +374,8 @@ def run_ours(args, cfg, rank, world, local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="c2", choices=sorted(synth.CONFIGS))
     ap.add_argument("--engine", default="auto", choices=["auto", "tc", "simt"])

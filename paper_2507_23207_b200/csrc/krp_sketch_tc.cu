@@ -107,30 +107,37 @@ __device__ __forceinline__ void sts_f32(uint32_t saddr, float v) {
 
 // One 8-column epilogue round for this thread's TMEM lane: z = D[rr..rr+8) (+ D[R8+rr..] for the concat
 // form), acc += z·Ω_S; on this side's T rounds, the 32-lane transposed butterfly of z·W is written to rbuf.
-// Shared memory is addressed through 32-bit shared-window addresses: wsw[j] = swizzled byte offset of
-// (row j mod 8, this lane) inside a W row block, so every load below is base + register + immediate.
+// w holds this lane's Khatri-Rao row W(lane, rr..rr+8) (registers, loaded once per segment); the Ω_S row of
+// the tile is read with two 16-byte loads (rows are R8 floats, zero padded).  Adds / fmas run two-wide.
 __device__ __forceinline__ void epi_round8(int rnd, float (&acc)[8], uint32_t tD, int R, int R8, int triple,
-                                           uint32_t oms_s, bool my_t, const uint32_t (&wsw)[8],
-                                           uint32_t rbuf_s, uint32_t sub, uint32_t lane) {
+                                           uint32_t oms_s, bool my_t, const float* w, uint32_t rbuf_s,
+                                           uint32_t sub, uint32_t lane) {
   const int rr = 8 * rnd;
-  float a[8], b[8], tv[8];
+  float a[8], b[8], om[8], tv[8];
   tmem_ld8(tD + rr, a);
   if (!triple) tmem_ld8(tD + R8 + rr, b);
+  lds_v4(oms_s + rr * 4, om[0], om[1], om[2], om[3]);
+  lds_v4(oms_s + rr * 4 + 16, om[4], om[5], om[6], om[7]);
   tmem_ld_wait();
+  const bool full = rr + 8 <= R;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const bool ok = rr + j < R;
-    const float z = ok ? (triple ? a[j] : a[j] + b[j]) : 0.f;
-    acc[j] = fmaf(z, ok ? lds_f32(oms_s + (rr + j) * 4) : 0.f, acc[j]);
-    tv[j] = z;
+  for (int j = 0; j < 8; j += 2) {
+    float2 z = make_float2(a[j], a[j + 1]);
+    if (!triple) z = f2_add(z, make_float2(b[j], b[j + 1]));
+    if (!full) {  // columns >= R of the accumulator hold padding (possibly stale TMEM): zero them
+      z.x = rr + j < R ? z.x : 0.f;
+      z.y = rr + j + 1 < R ? z.y : 0.f;
+    }
+    const float2 c = f2_fma(z, make_float2(om[j], om[j + 1]), make_float2(acc[j], acc[j + 1]));
+    acc[j] = c.x;
+    acc[j + 1] = c.y;
+    if (my_t) {
+      const float2 t = f2_mul(z, make_float2(w[j], w[j + 1]));
+      tv[j] = t.x;
+      tv[j + 1] = t.y;
+    }
   }
   if (my_t) {
-    const uint32_t lo_row = static_cast<uint32_t>(R8) * 128;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const uint32_t ad = wsw[j] + (rr + j) * 128;
-      tv[j] *= lds_f32(ad) + lds_f32(ad + lo_row);
-    }
     // 3 halving levels + 2 plain levels: lanes 4q..4q+3 end with the 32-lane sum for r = rr + q
 #pragma unroll
     for (int lvl = 0; lvl < 3; ++lvl) {
@@ -178,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < p.NS; ++i) {
       mbar_init(&full_x[i], 1);
-      mbar_init(&empty_x[i], kNumSplitWarps);
+      mbar_init(&empty_x[i], kNumSplitWarps + ((p.do_q && p.dbg != 1 && p.dbg != 4) ? 1 : 0));
     }
     for (int i = 0; i < p.NC; ++i) {
       mbar_init(&chunk_full[i], 4);
@@ -261,82 +268,105 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == kMmaWarp || warp == kMmaWarpQ) {
-    // ------------------------------------------------------------ MMA issuers: one thread per GEMM
+    // ------------------------------------------------------------ MMA issuers: one warp per GEMM
+    // The whole warp runs the loop (so every address / descriptor is warp-uniform and lives in uniform
+    // registers); one elected lane issues the tcgen05 instructions.  Descriptors are formed once and
+    // advanced by adding (byte offset >> 4) to the start-address field.
     const bool qgemm = (warp == kMmaWarpQ);
-    if (elect_one() && (qgemm ? p.do_q : p.do_p)) {
+    if (qgemm ? p.do_q : p.do_p) {
+      const bool leader = elect_one();
       const uint32_t idesc1 = make_idesc_tf32(128, p.NP, 0, 0);
       const uint32_t idesc2 = make_idesc_tf32(128, p.N2, 0, 0);
-      const uint32_t bp_addr = smem_u32(bp), bq_addr = smem_u32(bq);
-      int cst = 0, ast = 0;
+      const uint64_t bdesc0 = make_smem_desc(smem_u32(qgemm ? bq : bp), 0, 1024, kLayoutSW128);
+      const uint64_t adesc0 = make_smem_desc(smem_u32(xs), 0, 1024, kLayoutSW128);
+      const uint64_t lo_d = static_cast<uint64_t>(p.R8) * 8;        // B_lo rows start at R8: (R8*128 B) >> 4
+      const uint64_t katom_d = static_cast<uint64_t>(p.NP) * 8;     // one 32-wide K atom of B: (NP*128 B) >> 4
+      int cst = 0, ast = 0, xst = 0;
       uint32_t cph = 0, aph = 0, bph = 0;
-      int64_t prev_pair = -1;
+      int64_t s_cur = t0 % p.S;
+      bool first = true;
       for (int64_t t = t0; t < ((p.dbg == 1 || p.dbg == 4) ? t0 : t1); ++t) {
-        const int64_t pair = t / p.S;
-        if (pair != prev_pair) {
+        if (first || s_cur == 0) {  // a new (row block, col block) segment: wait for its B operands
           mbar_wait(b_ready, bph);
           bph ^= 1;
-          prev_pair = pair;
+          first = false;
         }
-        if (p.dbg == 0 || p.dbg == 5) mbar_wait(&acc_empty[ast], aph ^ 1);
-        KRP_TRACE(3, t - t0);
+        if (p.dbg == 0 || p.dbg == 5 || p.dbg >= 7) mbar_wait(&acc_empty[ast], aph ^ 1);
+        if (leader) KRP_TRACE(3, t - t0);
         tc_fence_after();
-        if (qgemm == !p.do_p) {  // Ω_S(s, :) for the epilogue, delivered on the same barrier as the accumulator
-          const int64_t s_ = t % p.S;
+        if (qgemm == !p.do_p && leader) {  // Ω_S(s, :) for the epilogue, on the same barrier as the accumulator
           mbar_arrive_expect_tx(&acc_full[ast], p.RS * 4);
-          bulk_copy_g2s(wsbuf + ast * p.RS, p.OmS + s_ * p.RS, p.RS * 4, &acc_full[ast]);
+          bulk_copy_g2s(wsbuf + ast * p.RS, p.OmS + s_cur * p.RS, p.RS * 4, &acc_full[ast]);
         }
-        const uint32_t dP = tbase + p.tm_acc + ast * 2 * p.DN;
-        const uint32_t dQ = dP + p.DN;
+        const uint32_t dacc = tbase + p.tm_acc + ast * 2 * p.DN + (qgemm ? p.DN : 0);
+        const uint64_t adesc_t = adesc0 + ((static_cast<uint64_t>(xst) * (kStageFloats * 4)) >> 4);
         for (int kc = 0; kc < nkc; ++kc) {
           mbar_wait(&chunk_full[cst], cph);
-          KRP_TRACE(10, (t - t0) * 8 + kc);
+          if (leader) KRP_TRACE(10 + (qgemm ? 2 : 0), (t - t0) * 8 + kc);
           tc_fence_after();
-          const uint32_t ch = tbase + p.tm_chunk + cst * 4 * CH;
-          if (p.dbg != 2) {
+          // A chunk in TMEM: P uses [hi | lo] at ch, ch + CH; Q uses lo at ch + 2 CH (hi from SMEM)
+          const uint32_t ach = tbase + p.tm_chunk + cst * 3 * CH + (qgemm ? 2 * CH : 0);
+          // first K-step of the chunk: kk0 = kc*CH/8; B atom kk0>>2, offset (kk0&3)*32 B
+          const int kk0 = kc * (CH / 8);
+          const uint64_t bchunk = bdesc0 + static_cast<uint64_t>(kk0 >> 2) * katom_d + (kk0 & 3) * 2;
+          const uint64_t achunk = adesc_t + static_cast<uint64_t>(kk0 >> 2) * 1024 + (kk0 & 3) * 2;  // 16 KB boxes
+          if (p.dbg != 2 && leader) {
+            if (p.triple) {
 #pragma unroll
-            for (int ks = 0; ks < CH / 8; ++ks) {
-              const int kk = kc * (CH / 8) + ks;
-              const uint32_t boff = (kk >> 2) * (p.NP * 128) + (kk & 3) * 32;
-              const uint32_t lo_off = p.R8 * 128;  // B_lo rows start at R8 (8-row aligned)
-              if (!qgemm) {
-                const uint64_t bd = make_smem_desc(bp_addr + boff, 0, 1024, kLayoutSW128);
-                if (p.triple) {
-                  const uint64_t bl = make_smem_desc(bp_addr + boff + lo_off, 0, 1024, kLayoutSW128);
-                  mma_tf32_ts(dP, ch + 0 * CH + 8 * ks, bd, idesc2, kk > 0 ? 1u : 0u);  // hi x hi
-                  mma_tf32_ts(dP, ch + 0 * CH + 8 * ks, bl, idesc2, 1u);                 // hi x lo
-                  mma_tf32_ts(dP, ch + 1 * CH + 8 * ks, bd, idesc2, 1u);                 // lo x hi
+              for (int ks = 0; ks < CH / 8; ++ks) {
+                const uint64_t bd = bchunk + ks * 2, bl = bd + lo_d;
+                const uint32_t acc0 = (kk0 + ks) > 0 ? 1u : 0u;
+                if (!qgemm) {
+                  mma_tf32_ts(dacc, ach + 8 * ks, bd, idesc2, acc0);       // hi x hi
+                  mma_tf32_ts(dacc, ach + 8 * ks, bl, idesc2, 1u);         // hi x lo
+                  mma_tf32_ts(dacc, ach + CH + 8 * ks, bd, idesc2, 1u);    // lo x hi
                 } else {
-                  mma_tf32_ts(dP, ch + 0 * CH + 8 * ks, bd, idesc1, kk > 0 ? 1u : 0u);  // hi x [B_hi | B_lo]
-                  mma_tf32_ts(dP, ch + 1 * CH + 8 * ks, bd, idesc2, 1u);                 // lo x B_hi
+                  const uint64_t ad = achunk + ks * 2;
+                  mma_tf32_ss(dacc, ad, bd, idesc2, acc0);
+                  mma_tf32_ss(dacc, ad, bl, idesc2, 1u);
+                  mma_tf32_ts(dacc, ach + 8 * ks, bd, idesc2, 1u);
                 }
               }
-              if (qgemm) {
-                const uint64_t bd = make_smem_desc(bq_addr + boff, 0, 1024, kLayoutSW128);
-                if (p.triple) {
-                  const uint64_t bl = make_smem_desc(bq_addr + boff + lo_off, 0, 1024, kLayoutSW128);
-                  mma_tf32_ts(dQ, ch + 2 * CH + 8 * ks, bd, idesc2, kk > 0 ? 1u : 0u);
-                  mma_tf32_ts(dQ, ch + 2 * CH + 8 * ks, bl, idesc2, 1u);
-                  mma_tf32_ts(dQ, ch + 3 * CH + 8 * ks, bd, idesc2, 1u);
+            } else {
+#pragma unroll
+              for (int ks = 0; ks < CH / 8; ++ks) {
+                const uint64_t bd = bchunk + ks * 2;
+                const uint32_t acc0 = (kk0 + ks) > 0 ? 1u : 0u;
+                if (!qgemm) {
+                  mma_tf32_ts(dacc, ach + 8 * ks, bd, idesc1, acc0);       // hi x [B_hi | B_lo]
+                  mma_tf32_ts(dacc, ach + CH + 8 * ks, bd, idesc2, 1u);    // lo x B_hi
                 } else {
-                  mma_tf32_ts(dQ, ch + 2 * CH + 8 * ks, bd, idesc1, kk > 0 ? 1u : 0u);
-                  mma_tf32_ts(dQ, ch + 3 * CH + 8 * ks, bd, idesc2, 1u);
+                  // A_hi = the raw fp32 tile straight from shared memory (K-major: K = ρ along the 128 B
+                  // rows of box kk/4, M = γ rows, SWIZZLE_128B, 8-row atoms 1 KB apart); the tensor core
+                  // reads it truncated to tf32, i.e. exactly hi.
+                  mma_tf32_ss(dacc, achunk + ks * 2, bd, idesc1, acc0);
+                  mma_tf32_ts(dacc, ach + 8 * ks, bd, idesc2, 1u);
                 }
               }
             }
           }
-          mma_commit(&chunk_empty[cst]);
-          KRP_TRACE(11, (t - t0) * 8 + kc);
+          if (leader) {
+            mma_commit(&chunk_empty[cst]);
+            KRP_TRACE(11 + (qgemm ? 2 : 0), (t - t0) * 8 + kc);
+          }
+          __syncwarp();
           if (++cst == p.NC) {
             cst = 0;
             cph ^= 1;
           }
         }
-        mma_commit(&acc_full[ast]);
-        KRP_TRACE(4, t - t0);
+        if (leader) {
+          if (qgemm) mma_commit(&empty_x[xst]);  // the raw tile may be overwritten once these MMAs finish
+          mma_commit(&acc_full[ast]);
+          KRP_TRACE(4, t - t0);
+        }
+        __syncwarp();
+        if (++xst == p.NS) xst = 0;
         if (++ast == p.NA) {
           ast = 0;
           aph ^= 1;
         }
+        if (++s_cur == p.S) s_cur = 0;
       }
     }
   } else if (warp < kNumSplitWarps) {
@@ -351,6 +381,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t cph = 0;
     const bool dop = p.do_p && p.dbg != 5 && p.dbg != 6, doq = p.do_q && p.dbg != 5 && p.dbg != 6;
     const int gq = static_cast<int>(32 * sub + lane);
+    // Shared-window addresses with the SWIZZLE_128B pattern folded in, so every load below is
+    // register + immediate.  P view: element (ρ = 32*sub + lane, γ) of box `sub` sits at byte
+    // γ*128 + (((lane>>2) ^ (γ&7)) << 4) + (lane&3)*4; γ&7 is a compile-time j&7 in the loop.
+    uint32_t psw[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      psw[j] = smem_u32(xs) + sub * 16384u + ((((lane >> 2) ^ static_cast<uint32_t>(j)) << 4) | ((lane & 3u) << 2));
+    // Q view: row γ = gq of box b holds ρ = 32b..32b+31; 16-byte chunk c of it sits at ((c ^ (gq&7)) << 4)
+    const uint32_t qrow = smem_u32(xs) + static_cast<uint32_t>(gq) * 128u;
+    const uint32_t qx = static_cast<uint32_t>(gq & 7);
     for (int64_t t = t0; t < t1; ++t) {
       mbar_wait(&full_x[xst], xph);
       if (sub == 0 && par == 0 && lane == 0) KRP_TRACE(1, t - t0);
@@ -367,43 +407,58 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&chunk_empty[my_cst], my_cph ^ 1);
         if (sub == 0 && lane == 0) KRP_TRACE(8, (t - t0) * 8 + kc);
         tc_fence_after();
-        const uint32_t ch = tbase + lane_off + p.tm_chunk + my_cst * 4 * CH;
-        // 16-column pieces keep the live register set small (CH may be 32)
-#pragma unroll 1
-        for (int h0 = 0; h0 < CH; h0 += 16) {
-          if (dop) {
-            // lane = ρ = 32*sub + lane (box `sub`), columns γ = kc*CH + h0 + j (rows of the box)
-            const float* box = X + sub * 4096;
-            uint32_t hi[16], lo[16];
+        const uint32_t ch = tbase + lane_off + p.tm_chunk + my_cst * 3 * CH;
+        const uint32_t stage_off = static_cast<uint32_t>(xst) * (kStageFloats * 4u);
+        // All shared-memory loads of the chunk are issued first (one load latency per chunk, not one per
+        // 16 columns), then hi / lo are formed and stored to TMEM with one 32x32b.xCH store each.
+        uint32_t px[CH];
+        float qv[CH];
+        if (dop && p.dbg == 8) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int g = kc * CH + h0 + j;
-              const float x = box[g * 32 + ((((lane >> 2) ^ (g & 7))) << 2) + (lane & 3)];
-              hi[j] = __float_as_uint(x);
-              lo[j] = __float_as_uint(x - __uint_as_float(tf32_hi_bits(x)));
-            }
-            tmem_st16(ch + 0 * CH + h0, hi);
-            tmem_st16(ch + 1 * CH + h0, lo);
+          for (int j = 0; j < CH; ++j) px[j] = __float_as_uint(1.0f + j);
+        }
+        if (dop && p.dbg != 8) {
+          // lane = ρ = 32*sub + lane (box `sub`), columns γ = kc*CH + j (rows of the box)
+          const uint32_t goff = stage_off + static_cast<uint32_t>(kc * CH) * 128u;
+#pragma unroll
+          for (int j = 0; j < CH; ++j) px[j] = __float_as_uint(lds_f32(psw[j & 7] + goff + static_cast<uint32_t>(j) * 128u));
+        }
+        if (doq && p.dbg == 7) {
+#pragma unroll
+          for (int j = 0; j < CH; ++j) qv[j] = 1.0f + j;
+        }
+        if (doq && p.dbg != 7) {
+          // lane = γ = 32*sub + lane, columns ρ = kc*CH + j: CH consecutive ρ of row γ (16-byte chunks)
+          const int rho0 = kc * CH;
+          const uint32_t rowa = qrow + stage_off + static_cast<uint32_t>(rho0 >> 5) * 16384u;
+#pragma unroll
+          for (int qq = 0; qq < CH / 4; ++qq) {
+            const uint32_t chunk = ((static_cast<uint32_t>(rho0 & 31) >> 2) + qq) ^ qx;
+            lds_v4(rowa + (chunk << 4), qv[4 * qq], qv[4 * qq + 1], qv[4 * qq + 2], qv[4 * qq + 3]);
           }
-          if (doq) {
-            // lane = γ = 32*sub + lane, columns ρ = kc*CH + h0 + j: 16 consecutive ρ of row γ
-            const int rho0 = kc * CH + h0;
-            const float* row = X + (rho0 >> 5) * 4096 + gq * 32;
-            uint32_t hi[16], lo[16];
+        }
+        if (dop) {
+          tmem_st<CH>(ch + 0 * CH, px);  // hi: the raw value (the tensor core truncates to tf32)
+          uint32_t lo[CH];
 #pragma unroll
-            for (int qq = 0; qq < 4; ++qq) {
-              const int chunk = (((rho0 & 31) >> 2) + qq) ^ (gq & 7);
-              const float4 v = *reinterpret_cast<const float4*>(row + chunk * 4);
-              const float vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                hi[qq * 4 + e] = __float_as_uint(vv[e]);
-                lo[qq * 4 + e] = __float_as_uint(vv[e] - __uint_as_float(tf32_hi_bits(vv[e])));
-              }
-            }
-            tmem_st16(ch + 2 * CH + h0, hi);
-            tmem_st16(ch + 3 * CH + h0, lo);
+          for (int j = 0; j < CH; j += 2) {
+            const float2 x = make_float2(__uint_as_float(px[j]), __uint_as_float(px[j + 1]));
+            const float2 l = f2_sub(x, make_float2(__uint_as_float(tf32_hi_bits(x.x)), __uint_as_float(tf32_hi_bits(x.y))));
+            lo[j] = __float_as_uint(l.x);
+            lo[j + 1] = __float_as_uint(l.y);
           }
+          tmem_st<CH>(ch + 1 * CH, lo);
+        }
+        if (doq) {
+          uint32_t lo[CH];
+#pragma unroll
+          for (int j = 0; j < CH; j += 2) {
+            const float2 l = f2_sub(make_float2(qv[j], qv[j + 1]),
+                                    make_float2(__uint_as_float(tf32_hi_bits(qv[j])), __uint_as_float(tf32_hi_bits(qv[j + 1]))));
+            lo[j] = __float_as_uint(l.x);
+            lo[j + 1] = __float_as_uint(l.y);
+          }
+          tmem_st<CH>(ch + 2 * CH, lo);
         }
         tmem_st_wait();
         if (sub == 0 && lane == 0) KRP_TRACE(9, (t - t0) * 8 + kc);
@@ -442,6 +497,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < 8; ++j) wsw[j] = wb + ((c0 ^ static_cast<uint32_t>(j)) << 4) + e0;
     }
     const uint32_t tA = tbase + lane_off + p.tm_a + (pside ? 0 : R8);  // A1 / A2 columns
+    // this lane's W row for this side's T rounds (P side: even rounds, Q side: odd rounds)
+    constexpr int kRounds = RA > 0 ? RA / 8 : kMaxTcR / 8;
+    constexpr int kTRounds = (kRounds + 1) / 2;
+    float wreg[8 * kTRounds];
+#pragma unroll
+    for (int j = 0; j < 8 * kTRounds; ++j) wreg[j] = 0.f;
     const uint32_t zero8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     float Areg[RA > 0 ? RA : 1];
 #pragma unroll
@@ -451,8 +512,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     int64_t prev_pair = -1;
     int seg = -1;
     int parity = 0;
-    for (int64_t t = t0; t < t1; ++t) {
-      const int64_t pair = t / p.S, s = t % p.S;
+    int64_t pair = t0 / p.S, s = t0 % p.S;  // advanced incrementally (no 64-bit division per tile)
+    for (int64_t t = t0; t < t1; ++t, (++s == p.S ? (s = 0, ++pair) : 0)) {
       if (pair != prev_pair) {
         if (prev_pair >= 0)
         {  // flush the finished segment's accumulators into its partial slot
@@ -498,8 +559,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_proxy_async_smem();
         named_bar_sync(1, kNumEpiWarps * 32);
         if (threadIdx.x == kEpiWarp0 * 32) mbar_arrive(b_ready);
+        if (p.do_t) {  // W(lane, r) = hi + lo rows of the image just copied (B_Q for the P side, B_P for Q)
+          const uint32_t lo_row = static_cast<uint32_t>(R8) * 128;
+#pragma unroll
+          for (int tr = 0; tr < kTRounds; ++tr) {
+            const int rr = 8 * (2 * tr + (pside ? 0 : 1));
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint32_t ad = wsw[j] + (rr + j) * 128;
+              wreg[8 * tr + j] = rr + j < R ? lds_f32(ad) + lds_f32(ad + lo_row) : 0.f;
+            }
+          }
+        }
       }
-      if (p.dbg != 0 && p.dbg != 5) continue;
+      if (p.dbg != 0 && p.dbg != 5 && p.dbg < 7) continue;
       mbar_wait(&acc_full[ast], aph);
       if (ew == 0 && lane == 0) KRP_TRACE(5, t - t0);
       tc_fence_after();
@@ -515,22 +588,25 @@ __global__ void __launch_bounds__(kThreads, 1)
               float acc8[8];  // register copies (no pointer into Areg, which must stay in registers)
 #pragma unroll
               for (int j = 0; j < 8; ++j) acc8[j] = Areg[8 * rnd + j];
-              epi_round8(rnd, acc8, tD, R, R8, p.triple, oms_s, p.do_t && ((rnd & 1) == (pside ? 0 : 1)), wsw, rbuf_s, sub,
-                         lane);
+              epi_round8(rnd, acc8, tD, R, R8, p.triple, oms_s, p.do_t && ((rnd & 1) == (pside ? 0 : 1)),
+                         &wreg[8 * (rnd >> 1)], rbuf_s, sub, lane);
 #pragma unroll
               for (int j = 0; j < 8; ++j) Areg[8 * rnd + j] = acc8[j];
             }
           }
         } else {
-          for (int rnd = 0; rnd < nr; ++rnd) {
-            float acc[8];
-            tmem_ld8(tA + 8 * rnd, acc);
-            epi_round8(rnd, acc, tD, R, R8, p.triple, oms_s, p.do_t && ((rnd & 1) == (pside ? 0 : 1)), wsw, rbuf_s, sub,
-                       lane);
-            uint32_t accb[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) accb[j] = __float_as_uint(acc[j]);
-            tmem_st8(tA + 8 * rnd, accb);
+          for (int rnd = 0; rnd < kRounds; ++rnd) {
+            if (rnd < nr) {
+              float acc[8];
+              tmem_ld8(tA + 8 * rnd, acc);
+              epi_round8(rnd, acc, tD, R, R8, p.triple, oms_s, p.do_t && ((rnd & 1) == (pside ? 0 : 1)),
+                         &wreg[8 * (rnd >> 1)], rbuf_s, sub, lane);
+              uint32_t accb[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) accb[j] = __float_as_uint(acc[j]);
+              tmem_st8(tA + 8 * rnd, accb);
+            }
           }
           tmem_st_wait();
         }
@@ -653,35 +729,81 @@ struct RedParams {
   float *Pm, *Qc, *Ts;
 };
 
-// P(ρ,r) = Σ_{cb} Σ_{CTAs b of pair (rb,cb)} partA1[slot(b,pair)][ρ%128][r]   (fixed order)
-// Qc(γ,r) likewise over rb;  Ts(s,r) = Σ_{pairs} Tpart[pair][s][r]
-__global__ void tc_assemble_kernel(const __grid_constant__ RedParams p) {
-  int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+// P(ρ,r) = Σ_{cb} Σ_{CTAs b of pair (rb,cb)} partA1[slot(b,pair)][ρ%128][r]
+// Qc(γ,r) likewise over rb;  Ts(s,r) = Σ_{pairs} Tpart[pair][s][r].
+// One block = 32 consecutive outputs (lanes, coalesced) x 8 warps; warp w sums its fixed share of the
+// terms in order, then warp 0 adds the 8 warp sums in order: a fixed reduction tree (deterministic)
+// whose depth is terms/8 instead of terms.  A block never straddles a 128-row block (32 | 128*R) nor
+// a region (regions are padded to whole blocks).
+constexpr int kRedWarps = 8;
+__global__ void __launch_bounds__(256) tc_assemble_kernel(const __grid_constant__ RedParams p) {
+  __shared__ float red[kRedWarps][32];
+  const int w = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
   const int64_t nP = p.do_p ? p.M * p.R : 0, nQ = p.do_q ? p.C * p.R : 0, nT = p.do_t ? p.S * p.R : 0;
-  if (idx < nP + nQ) {
-    const bool rows = idx < nP;
-    if (!rows) idx -= nP;
-    const int64_t lin = idx / p.R;
-    const int r = static_cast<int>(idx - lin * p.R);
+  const int64_t bP = (nP + 31) / 32, bQ = (nQ + 31) / 32;
+  int64_t blk_id = blockIdx.x;
+  int region;
+  if (blk_id < bP) {
+    region = 0;
+  } else if ((blk_id -= bP) < bQ) {
+    region = 1;
+  } else {
+    blk_id -= bQ;
+    region = 2;
+  }
+  const int64_t idx = blk_id * 32 + lane;
+  float acc = 0.f;
+  if (region < 2) {
+    const bool rows = region == 0;
+    const int64_t n = rows ? nP : nQ;
+    const int64_t lin = (idx < n ? idx : n - 1) / p.R;
+    const int r = static_cast<int>((idx < n ? idx : n - 1) - lin * p.R);
     const int blk = static_cast<int>(lin / kTile), l = static_cast<int>(lin % kTile);
     const float* part = rows ? p.partA1 : p.partA2;
     const int nother = rows ? p.CB : p.RB;
-    float acc = 0.f;
+    const int64_t kstride = static_cast<int64_t>(kTile) * p.R;
     for (int o = 0; o < nother; ++o) {
       const int64_t pair = rows ? (static_cast<int64_t>(blk) * p.CB + o) : (static_cast<int64_t>(o) * p.CB + blk);
       const int nk = cta_of_tile((pair + 1) * p.S - 1, p.T, p.grid) - cta_of_tile(pair * p.S, p.T, p.grid) + 1;
+      const int k0 = w * nk / kRedWarps, k1 = (w + 1) * nk / kRedWarps;
       const float* src = part + ((pair * p.maxseg) * kTile + l) * p.R + r;
-      for (int k = 0; k < nk; ++k) acc += src[static_cast<int64_t>(k) * kTile * p.R];
+      for (int k = k0; k < k1; k += 8) {
+        float v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = (k + i < k1) ? __ldg(src + (k + i) * kstride) : 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc += v[i];
+      }
     }
-    (rows ? p.Pm : p.Qc)[idx] = acc;
-  } else if ((idx -= nP + nQ) < nT) {
-    const int64_t s = idx / p.R;
-    const int r = static_cast<int>(idx - s * p.R);
+  } else {
+    const int64_t idc = idx < nT ? idx : nT - 1;
+    const int64_t s = idc / p.R;
+    const int r = static_cast<int>(idc - s * p.R);
     const int64_t npairs = static_cast<int64_t>(p.RB) * p.CB;
-    float acc = 0.f;
-    for (int64_t pr = 0; pr < npairs; ++pr) acc += p.Tpart[(pr * p.S + s) * p.R + r];
-    p.Ts[idx] = acc;
+    const int64_t p0 = w * npairs / kRedWarps, p1 = (w + 1) * npairs / kRedWarps;
+    const int64_t pstride = p.S * p.R;
+    const float* src = p.Tpart + s * p.R + r;
+    for (int64_t q = p0; q < p1; q += 8) {
+      float v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = (q + i < p1) ? __ldg(src + (q + i) * pstride) : 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc += v[i];
+    }
   }
+  red[w][lane] = acc;
+  __syncthreads();
+  if (w == 0) {
+    float tot = red[0][lane];
+#pragma unroll
+    for (int i = 1; i < kRedWarps; ++i) tot += red[i][lane];
+    const int64_t n = region == 0 ? nP : (region == 1 ? nQ : nT);
+    if (idx < n) (region == 0 ? p.Pm : (region == 1 ? p.Qc : p.Ts))[idx] = tot;
+  }
+}
+
+int64_t assemble_blocks(int64_t M, int64_t C, int64_t S, int R, int do_p, int do_q, int do_t) {
+  return (do_p ? (M * R + 31) / 32 : 0) + (do_q ? (C * R + 31) / 32 : 0) + (do_t ? (S * R + 31) / 32 : 0);
 }
 
 struct TtvParams {
@@ -695,44 +817,70 @@ struct TtvParams {
   int want[kMaxD];
 };
 
-// Y_k(i, r) = Σ_{lin: i_k(lin) = i} src(lin, r) Π_{j in group, j != k} Ω_j(i_j(lin), r)
-__global__ void tc_ttv_kernel(const __grid_constant__ TtvParams p) {
-  int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  for (int k = 0; k < p.d; ++k) {
+// Y_k(i, r) = Σ_{lin: i_k(lin) = i} src(lin, r) Π_{j in group, j != k} Ω_j(i_j(lin), r)   (fp64 sums)
+// Same block shape as the assembly: 32 outputs x 8 warps splitting the o range, fixed-order combine.
+__global__ void __launch_bounds__(256) tc_ttv_kernel(const __grid_constant__ TtvParams p) {
+  __shared__ double red[kRedWarps][32];
+  const int w = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
+  int64_t blk_id = blockIdx.x;
+  int k = 0;
+  int64_t cnt = 0;
+  for (k = 0; k < p.d; ++k) {
     if (!p.want[k]) continue;
-    const int64_t cnt = p.n[k] * p.R;
-    if (idx >= cnt) {
-      idx -= cnt;
-      continue;
-    }
-    const int64_t i = idx / p.R;
-    const int r = static_cast<int>(idx - i * p.R);
-    int g0, g1;
-    const float* src;
-    int64_t gsize;
-    if (k < p.m) {
-      g0 = 0, g1 = p.m, src = p.Pm, gsize = p.M;
-    } else if (k < p.m2) {
-      g0 = p.m, g1 = p.m2, src = p.Qc, gsize = p.C;
-    } else {
-      g0 = p.m2, g1 = p.d, src = p.Ts, gsize = p.S;
-    }
-    const int64_t others = gsize / p.n[k];
-    double acc = 0.0;
-    for (int64_t o = 0; o < others; ++o) {
-      int64_t rem = o, lin = i * p.gs[k];
-      float w = 1.f;
-      for (int j = g0; j < g1; ++j) {
-        if (j == k) continue;
-        const int64_t ij = rem % p.n[j];
-        rem /= p.n[j];
-        lin += ij * p.gs[j];
-        w *= __ldg(p.om[j] + ij * p.R + r);
+    cnt = p.n[k] * p.R;
+    const int64_t nb = (cnt + 31) / 32;
+    if (blk_id < nb) break;
+    blk_id -= nb;
+  }
+  if (k >= p.d) return;
+  const int64_t idx = blk_id * 32 + lane;
+  const int64_t idc = idx < cnt ? idx : cnt - 1;
+  const int64_t i = idc / p.R;
+  const int r = static_cast<int>(idc - i * p.R);
+  int g0, g1;
+  const float* src;
+  int64_t gsize;
+  if (k < p.m) {
+    g0 = 0, g1 = p.m, src = p.Pm, gsize = p.M;
+  } else if (k < p.m2) {
+    g0 = p.m, g1 = p.m2, src = p.Qc, gsize = p.C;
+  } else {
+    g0 = p.m2, g1 = p.d, src = p.Ts, gsize = p.S;
+  }
+  const int64_t others = gsize / p.n[k];
+  const int64_t o0 = w * others / kRedWarps, o1 = (w + 1) * others / kRedWarps;
+  double acc = 0.0;
+  for (int64_t ob = o0; ob < o1; ob += 4) {
+    float xv[4], wv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      xv[u] = 0.f;
+      wv[u] = 0.f;
+      const int64_t o = ob + u;
+      if (o < o1) {
+        int64_t rem = o, lin = i * p.gs[k];
+        float wt = 1.f;
+        for (int j = g0; j < g1; ++j) {
+          if (j == k) continue;
+          const int64_t ij = rem % p.n[j];
+          rem /= p.n[j];
+          lin += ij * p.gs[j];
+          wt *= __ldg(p.om[j] + ij * p.R + r);
+        }
+        xv[u] = __ldg(src + lin * p.R + r);
+        wv[u] = wt;
       }
-      acc += static_cast<double>(src[lin * p.R + r]) * w;
     }
-    p.y[k][i * p.R + r] = static_cast<float>(acc);
-    return;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc += static_cast<double>(xv[u]) * wv[u];
+  }
+  red[w][lane] = acc;
+  __syncthreads();
+  if (w == 0) {
+    double tot = red[0][lane];
+#pragma unroll
+    for (int u = 1; u < kRedWarps; ++u) tot += red[u][lane];
+    if (idx < cnt) p.y[k][i * p.R + r] = static_cast<float>(tot);
   }
 }
 
@@ -806,7 +954,7 @@ bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, TcPlan& pl
   pl.do_p = (wr || ws) ? 1 : 0;  // T rounds alternate between z1 (P side) and z2 (Q side)
   pl.do_q = (wc || ws) ? 1 : 0;
   pl.R8 = (R + 7) / 8 * 8;
-  pl.RS = (R + 3) / 4 * 4;
+  pl.RS = (R + 7) / 8 * 8;  // Ω_S rows padded to R8 (zeros) so the epilogue reads them as 16-byte vectors
   pl.N2 = round16(R);
   // TMEM (512 columns): NA accumulator stages of 2*DN, NC A-chunk stages of 4*CH, and A1 + A2 (2*R8) when
   // they do not live in registers.  The [hi|lo] concat form is 2 MMAs per K-step (DN = round16(R8 + R)),
@@ -814,20 +962,25 @@ bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, TcPlan& pl
   {
     struct Opt {
       int triple, na, ch, ncmin, areg;
-    } opts[5] = {{0, 2, 32, 2, 1}, {1, 2, 32, 2, 1}, {0, 2, 16, 3, 0}, {1, 2, 16, 2, 0}, {1, 1, 16, 2, 0}};
+    } opts[8] = {{0, 2, 16, 4, 1}, {0, 2, 32, 2, 1}, {1, 2, 32, 2, 1}, {0, 2, 32, 2, 0},
+                 {0, 2, 16, 3, 0}, {1, 2, 32, 2, 0}, {1, 2, 16, 2, 0}, {1, 1, 16, 2, 0}};
     pl.NC = 0;
-    for (const Opt& o : opts) {
+    const char* force = getenv("KRP_TC_OPT");  // development: force one option (if it fits)
+    const int fo = force ? atoi(force) : -1;
+    for (int oi = 0; oi < 8; ++oi) {
+      const Opt& o = opts[oi];
+      if (fo >= 0 && oi != fo) continue;
       if (o.areg && pl.R8 > 48) continue;  // register accumulators up to R = 48
       const int dn = o.triple ? pl.N2 : round16(pl.R8 + R);
       const int acols = o.areg ? 0 : 2 * pl.R8;
-      const int nc = std::min(4, (512 - o.na * 2 * dn - acols) / (4 * o.ch));
+      const int nc = std::min(o.ch == 16 ? 6 : 4, (512 - o.na * 2 * dn - acols) / (3 * o.ch));
       if (nc >= o.ncmin) {
         pl.triple = o.triple;
         pl.DN = dn;
         pl.NA = o.na;
         pl.CH = o.ch;
         pl.NC = nc;
-        pl.RA = o.areg ? (pl.R8 <= 16 ? 16 : (pl.R8 <= 32 ? 32 : 48)) : 0;
+        pl.RA = o.areg ? pl.R8 : 0;
         break;
       }
     }
@@ -836,7 +989,7 @@ bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, TcPlan& pl
   }
   pl.tm_acc = 0;
   pl.tm_chunk = pl.NA * 2 * pl.DN;
-  pl.tm_a = pl.tm_chunk + pl.NC * 4 * pl.CH;
+  pl.tm_a = pl.tm_chunk + pl.NC * 3 * pl.CH;
   // SMEM: X stages (64 KB each), B_P and B_Q (NP rows x 512 B each), reduction scratch, barriers
   const uint32_t bbytes = static_cast<uint32_t>(pl.NP) * 512u;
   const uint32_t misc = 2 * 4 * kMaxTcR * 4 + 256 + 2 * kMaxTcR * 4;
@@ -1069,10 +1222,22 @@ int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const b
     KRP_CHECK_LAUNCH();
   }
   // 2. the fused tile kernel
-  auto kern = (pl.CH == 32)   ? (pl.RA == 16 ? krp_tc_sketch_kernel<32, 16>
-                                 : pl.RA == 32 ? krp_tc_sketch_kernel<32, 32>
-                                               : krp_tc_sketch_kernel<32, 48>)
-                              : krp_tc_sketch_kernel<16, 0>;
+  using KernFn = void (*)(const CUtensorMap, const TcParams);
+  // register-accumulator variants are sized to R8 exactly (register pressure), all with CH = 32
+  KernFn kern = nullptr;
+  if (pl.RA == 0) {
+    kern = pl.CH == 32 ? krp_tc_sketch_kernel<32, 0> : krp_tc_sketch_kernel<16, 0>;
+  } else {
+    const bool c32 = pl.CH == 32;
+    switch (pl.RA) {
+      case 8: kern = c32 ? krp_tc_sketch_kernel<32, 8> : krp_tc_sketch_kernel<16, 8>; break;
+      case 16: kern = c32 ? krp_tc_sketch_kernel<32, 16> : krp_tc_sketch_kernel<16, 16>; break;
+      case 24: kern = c32 ? krp_tc_sketch_kernel<32, 24> : krp_tc_sketch_kernel<16, 24>; break;
+      case 32: kern = c32 ? krp_tc_sketch_kernel<32, 32> : krp_tc_sketch_kernel<16, 32>; break;
+      case 40: kern = c32 ? krp_tc_sketch_kernel<32, 40> : krp_tc_sketch_kernel<16, 40>; break;
+      default: kern = c32 ? krp_tc_sketch_kernel<32, 48> : krp_tc_sketch_kernel<16, 48>; break;
+    }
+  }
   KRP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(pl.smem_bytes)));
   prof_begin(s);
@@ -1109,8 +1274,8 @@ int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const b
     rp.Pm = Pm;
     rp.Qc = Qc;
     rp.Ts = Ts;
-    const int64_t nasm = (pl.do_p ? pl.M * R : 0) + (pl.do_q ? pl.C * R : 0) + (pl.do_t ? pl.S * R : 0);
-    tc_assemble_kernel<<<static_cast<unsigned>((nasm + 255) / 256), 256, 0, s>>>(rp);
+    const int64_t nblk = assemble_blocks(pl.M, pl.C, pl.S, R, pl.do_p, pl.do_q, pl.do_t);
+    tc_assemble_kernel<<<static_cast<unsigned>(nblk), 256, 0, s>>>(rp);
     KRP_CHECK_LAUNCH();
   }
   {
@@ -1129,12 +1294,12 @@ int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const b
       tv.om[k] = om.p[k];
       tv.want[k] = want[k] ? 1 : 0;
       tv.y[k] = want[k] ? Y[k] : nullptr;
-      if (want[k]) nout += g.n[k] * R;
+      if (want[k]) nout += (g.n[k] * R + 31) / 32;
     }
     tv.Pm = Pm;
     tv.Qc = Qc;
     tv.Ts = Ts;
-    tc_ttv_kernel<<<static_cast<unsigned>((nout + 255) / 256), 256, 0, s>>>(tv);
+    tc_ttv_kernel<<<static_cast<unsigned>(nout), 256, 0, s>>>(tv);
     KRP_CHECK_LAUNCH();
   }
   ar.off = mark;

@@ -60,9 +60,45 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Blocking wait: try_wait with a suspend-time hint lets the hardware park the warp until the phase
+// completes (or ~10 ms pass) instead of re-issuing the probe, so waiting warps do not steal issue slots
+// from the warps that do the work.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "KRP_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n\t"
+      "@!p bra KRP_WAIT;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// ----------------------------------------------------------------- packed fp32x2 arithmetic
+// sm_100 issues two fp32 adds / muls / fmas per instruction (FADD2 / FMUL2 / FFMA2).
+#define SM100_F2_OP2(name, op)                                                                    \
+  __device__ __forceinline__ float2 name(float2 a, float2 b) {                                  \
+    float2 d;                                                                                   \
+    asm("{\n\t.reg .b64 a2, b2, d2;\n\tmov.b64 a2, {%2, %3};\n\tmov.b64 b2, {%4, %5};\n\t" op \
+        " d2, a2, b2;\n\tmov.b64 {%0, %1}, d2;\n\t}"                                            \
+        : "=f"(d.x), "=f"(d.y)                                                                  \
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));                                              \
+    return d;                                                                                   \
   }
+SM100_F2_OP2(f2_add, "add.rn.f32x2")
+SM100_F2_OP2(f2_sub, "sub.rn.f32x2")
+SM100_F2_OP2(f2_mul, "mul.rn.f32x2")
+#undef SM100_F2_OP2
+// d = a * b + c
+__device__ __forceinline__ float2 f2_fma(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 a2, b2, c2, d2;\n\tmov.b64 a2, {%2, %3};\n\tmov.b64 b2, {%4, %5};\n\tmov.b64 c2, {%6, %7};\n\t"
+      "fma.rn.f32x2 d2, a2, b2, c2;\n\tmov.b64 {%0, %1}, d2;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ void lds_v4(uint32_t saddr, float& a, float& b, float& c, float& d) {
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "r"(saddr));
 }
 
 // ----------------------------------------------------------------- proxies / fences

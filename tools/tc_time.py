@@ -14,7 +14,7 @@ omn = synth.omegas(dims, cfg.R, 2)
 om = [torch.from_numpy(o).cuda() for o in omn]
 ws = torch.empty(krp.krp_workspace_bytes(krp.OP_SKETCH_ALL, dims, cfg.R), dtype=torch.uint8, device='cuda')
 Y = [torch.empty((n, cfg.R), device='cuda') for n in dims]
-for _ in range(3):
+for _ in range(3 if len(sys.argv) < 5 else 0):
     krp.krp_sketch_all_modes(x, dims, om, Y=Y, ws=ws)
 torch.cuda.synchronize()
 krp.krp_profile_reset(); krp.krp_profile_enable(True)
