@@ -146,11 +146,17 @@ def _calibrate_slabs(cfg, seed, om, target_s):
 
 
 def cpu_baseline(cfg, seed, om, target_s=12.0):
+    """The oracle as it stands, on a bounded sample of the workload: last-mode slabs [0, slabs) sized to
+    ~target_s of CPU work; when the whole tensor takes less, the whole-tensor sketch is repeated."""
     slabs = _calibrate_slabs(cfg, seed, om, target_s)
     t, f = _oracle_sample(cfg, seed, slabs, om)
-    return {"value": f / t / 1e12, "unit": "TFLOP/s", "cores": _cores(), "kind": "oracle",
+    reps = 1
+    if slabs == cfg.dims[-1] and t < 0.5 * target_s:
+        reps = max(1, int(round(target_s / max(t, 1e-3))))
+        t = sum(_oracle_sample(cfg, seed, slabs, om)[0] for _ in range(reps))
+    return {"value": f * reps / t / 1e12, "unit": "TFLOP/s", "cores": _cores(), "kind": "oracle",
             "sample": f"fp64 numpy explicit-KR all-mode sketch of last-mode slabs [0,{slabs}) of {cfg.name} "
-                      f"({slabs}/{cfg.dims[-1]} of the tensor, {t:.1f} s, os.cpu_count()={os.cpu_count()})"}
+                      f"({slabs}/{cfg.dims[-1]} of the tensor) x{reps}, {t:.1f} s, os.cpu_count()={os.cpu_count()}"}
 
 
 # ------------------------------------------------------------------ reference arm
@@ -194,7 +200,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     torch.cuda.set_device(dev)
     krp.krp_set_engine({"auto": 0, "tc": 1, "simt": 2}[args.engine])
     Id = cfg.dims[-1]
-    k0, k1 = rank * Id // world, (rank + 1) * Id // world
+    k0, kn = krp.krp_slab_range(Id, world, rank)  # the library's slab geometry
+    k1 = k0 + kn
     dims_local = list(cfg.dims[:-1]) + [k1 - k0]
     n_local = int(np.prod(dims_local))
     x_host = torch.from_numpy(synth.tensor_slab(cfg, args.seed, k0, k1)).pin_memory()

@@ -141,6 +141,21 @@ KRP_API int krp_sketch_all_modes_dist(const float* X_slab, int d, const int64_t*
 KRP_API int krp_rhosvd_dist(const float* X_slab, int d, const int64_t* dims_local, int64_t I_d_global, int64_t slab_begin,
                     const int* ranks, int R, const float* const* omega, float* const* Q, float* core,
                     double* rel_err, void* ws, size_t ws_bytes, krp_comm comm, void* stream);
+/* Host-side sharding geometry (pure host functions, no device access; used by the _dist calls and by
+ * callers that place the slabs).  SURVEY §8(e): rank g of G owns the contiguous last-mode index range
+ * [begin, begin + len) with begin = floor(g * I_d / G) (balanced, ragged when G does not divide I_d).
+ * Returns KRP_EINVAL for I_d < 1, nranks < 1 or rank outside [0, nranks). */
+KRP_API int krp_slab_range(int64_t I_d, int nranks, int rank, int64_t* begin, int64_t* len);
+
+/* Layout of the packed buffer that the sharded sketch combines with ONE all-reduce(sum):
+ * [Y_1 | Y_2 | ... | Y_{d-1} | Y_d], each I_n x R row-major, Y_d with the GLOBAL I_d rows; a rank writes
+ * its partial Y_1..Y_{d-1} and only its own slab rows of Y_d (zeros elsewhere), so the sum both adds the
+ * partials and gathers the slab rows.  offsets[n] (n = 0..d-1) = float offset of Y_{n+1}; offsets[d] =
+ * total floats; *slab_offset = float offset of this rank's first Y_d row.  dims_local[d-1] is the slab
+ * length.  Returns KRP_EINVAL / KRP_ESHAPE on bad arguments. */
+KRP_API int krp_pack_layout(int d, const int64_t* dims_local, int64_t I_d_global, int64_t slab_begin, int R,
+                            int64_t* offsets, int64_t* slab_offset);
+
 /* Workspace for the _dist calls: krp_workspace_bytes(op, d, dims_local, R, ranks) with the global
  * last-mode size passed through this helper. */
 KRP_API size_t krp_workspace_bytes_dist(int op, int d, const int64_t* dims_local, int64_t I_d_global, int R,

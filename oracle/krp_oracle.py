@@ -38,6 +38,7 @@ __all__ = [
     "sketch_mode",
     "sketch_all_modes",
     "sketch_mode_rows",
+    "sketch_rows_ttv",
     "thin_qr",
     "ttm",
     "multi_ttm",
@@ -157,6 +158,32 @@ def sketch_mode_rows(flat: np.ndarray, dims: Sequence[int], omegas: Sequence[np.
         xu = unfold(slab, n)  # I_n x prod_{m<d-1, m!=n} I_m
         for t, i in enumerate(rows):
             out[t] += (xu[i] @ w_in) * np.asarray(omegas[d - 1][k], dtype=np.float64)
+    return out
+
+
+def sketch_rows_ttv(flat: np.ndarray, dims: Sequence[int], omegas: Sequence[np.ndarray], n: int,
+                    rows: Sequence[int]) -> np.ndarray:
+    """Rows ``rows`` of Y_n by the column identity Y_n(i, j) = (X ×_{k≠n} ω_k^(j)ᵀ)(i)  (column
+    j of Ω_d ⊙ ⋯ ⊙ Ω_1 is ω_d^(j) ⊗ ⋯ ⊗ ω_1^(j), so the MTTKRP column is a multi-TTV).
+
+    For each requested i it gathers the sub-tensor X(i_n = i) from the flat fp32 buffer (no full fp64
+    copy of X) and contracts the remaining modes one at a time, keeping the column index j diagonal:
+    T(j, ...) <- Σ_{i_k} T(j, i_k, ...) Ω_k(i_k, j).  Used for sampled parity at full BASELINE sizes,
+    where the explicit Khatri-Rao product does not fit in memory."""
+    dims = tuple(int(v) for v in dims)
+    d = len(dims)
+    R = np.asarray(omegas[(n + 1) % d]).shape[1]
+    x = np.asarray(flat).reshape(dims[::-1])  # C-order view: axis a holds mode d-1-a (first index fastest)
+    out = np.zeros((len(rows), R))
+    others = [k for k in range(d) if k != n]
+    for t, i in enumerate(rows):
+        sub = np.asarray(np.take(x, int(i), axis=d - 1 - n), dtype=np.float64)  # axes: modes others[::-1]
+        # contract the slowest remaining mode first (leading axis), keeping j as the leading axis
+        k = others[-1]
+        T = np.einsum("a...,aj->j...", sub, np.asarray(omegas[k], dtype=np.float64))
+        for k in others[-2::-1]:
+            T = np.einsum("ja...,aj->j...", T, np.asarray(omegas[k], dtype=np.float64))
+        out[t] = T
     return out
 
 

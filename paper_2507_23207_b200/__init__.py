@@ -23,7 +23,7 @@ __all__ = [
     "OP_RHOSVD_ERR", "ENGINE_AUTO", "ENGINE_TC", "ENGINE_SIMT", "krp_set_engine", "krp_workspace_bytes",
     "krp_sketch_all_modes", "krp_sketch_all_modes_host", "krp_sketch_mode", "krp_rhosvd", "krp_sthosvd",
     "krp_launch_count", "krp_reset_launch_count", "Comm", "krp_sketch_all_modes_dist", "krp_rhosvd_dist",
-    "krp_workspace_bytes_dist", "EXPORTED_SYMBOLS", "LIB_PATH",
+    "krp_workspace_bytes_dist", "EXPORTED_SYMBOLS", "LIB_PATH", "krp_slab_range", "krp_pack_layout",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libkrp.so")
@@ -37,6 +37,7 @@ EXPORTED_SYMBOLS = [
     "krp_comm_id_bytes", "krp_comm_get_unique_id", "krp_comm_init", "krp_comm_destroy",
     "krp_sketch_all_modes_dist", "krp_rhosvd_dist", "krp_workspace_bytes_dist", "krp_launch_count",
     "krp_reset_launch_count", "krp_profile_enable", "krp_profile_read", "krp_profile_reset",
+    "krp_slab_range", "krp_pack_layout",
 ]
 
 _lib = None
@@ -87,6 +88,8 @@ def lib() -> ctypes.CDLL:
                                                  ctypes.c_int, ptrs, _P, ctypes.c_size_t, _P, _P]
         l_.krp_rhosvd_dist.argtypes = [_P, ctypes.c_int, _I64P, ctypes.c_int64, ctypes.c_int64, _IP, ctypes.c_int,
                                        ptrs, ptrs, _P, ctypes.POINTER(ctypes.c_double), _P, ctypes.c_size_t, _P, _P]
+        l_.krp_slab_range.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int, _I64P, _I64P]
+        l_.krp_pack_layout.argtypes = [ctypes.c_int, _I64P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, _I64P, _I64P]
         l_.krp_launch_count.restype = ctypes.c_uint64
         l_.krp_profile_enable.argtypes = [ctypes.c_int]
         l_.krp_profile_read.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64),
@@ -252,6 +255,24 @@ def krp_sthosvd(X: torch.Tensor, dims: Sequence[int], ranks: Sequence[int],
 
 
 # ------------------------------------------------------------------ multi-GPU
+def krp_slab_range(I_d: int, nranks: int, rank: int) -> Tuple[int, int]:
+    """(begin, length) of rank's contiguous last-mode slab (host-side geometry of the sharded path)."""
+    b, n = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().krp_slab_range(int(I_d), int(nranks), int(rank), ctypes.byref(b), ctypes.byref(n)),
+           "krp_slab_range")
+    return b.value, n.value
+
+
+def krp_pack_layout(dims_local: Sequence[int], I_d_global: int, slab_begin: int, R: int) -> Tuple[List[int], int]:
+    """(offsets[0..d], slab_offset) of the packed all-reduce buffer [Y_1 | ... | Y_d] (floats)."""
+    d = len(dims_local)
+    offs = (ctypes.c_int64 * (d + 1))()
+    so = ctypes.c_int64()
+    _check(lib().krp_pack_layout(d, _dims(dims_local), int(I_d_global), int(slab_begin), int(R), offs,
+                                 ctypes.byref(so)), "krp_pack_layout")
+    return list(offs), so.value
+
+
 class Comm:
     """NCCL communicator owned by libkrp, bootstrapped through a torch.distributed process group."""
 

@@ -942,6 +942,34 @@ static int validate_slab(int d, const int64_t* dims_local, int64_t Id_global, in
   return KRP_OK;
 }
 
+int krp_slab_range(int64_t I_d, int nranks, int rank, int64_t* begin, int64_t* len) {
+  if (I_d < 1 || nranks < 1 || rank < 0 || rank >= nranks || !begin || !len) {
+    set_error("krp_slab_range: bad arguments");
+    return KRP_EINVAL;
+  }
+  const int64_t b = I_d * rank / nranks, e = I_d * (rank + 1) / nranks;
+  *begin = b;
+  *len = e - b;
+  return KRP_OK;
+}
+
+int krp_pack_layout(int d, const int64_t* dims_local, int64_t I_d_global, int64_t slab_begin, int R,
+                    int64_t* offsets, int64_t* slab_offset) {
+  if (!dims_local || !offsets || !slab_offset || d < 2 || d > krp::kMaxD || R < 1) {
+    set_error("krp_pack_layout: bad arguments");
+    return KRP_EINVAL;
+  }
+  KRP_TRY(validate_slab(d, dims_local, I_d_global, slab_begin));
+  int64_t off = 0;
+  for (int k = 0; k < d; ++k) {
+    offsets[k] = off;
+    off += ((k == d - 1) ? I_d_global : dims_local[k]) * R;
+  }
+  offsets[d] = off;
+  *slab_offset = offsets[d - 1] + slab_begin * R;
+  return KRP_OK;
+}
+
 int krp_sketch_all_modes_dist(const float* X_slab, int d, const int64_t* dims_local, int64_t I_d_global,
                               int64_t slab_begin, const float* const* omega, int R, float* const* Y, void* ws,
                               size_t ws_bytes, krp_comm comm, void* stream) {
@@ -959,17 +987,13 @@ int krp_sketch_all_modes_dist(const float* X_slab, int d, const int64_t* dims_lo
   WsGuard guard;
   KRP_TRY(setup_arena(krp_workspace_bytes_dist(KRP_OP_SKETCH_ALL, d, dims_local, I_d_global, R, nullptr), ws,
                       ws_bytes, s, ar, guard));
-  int64_t ysum = 0;
-  for (int k = 0; k < d - 1; ++k) ysum += dims_local[k] * R;
-  ysum += I_d_global * R;
+  int64_t poff[kMaxD + 1], slab_off = 0;
+  KRP_TRY(krp_pack_layout(d, dims_local, I_d_global, slab_begin, R, poff, &slab_off));
+  const int64_t ysum = poff[d];
   float* pack = ar.take<float>(ysum);
   float* Yl[kMaxD];
-  int64_t off = 0;
-  for (int k = 0; k < d - 1; ++k) {
-    Yl[k] = pack + off;
-    off += dims_local[k] * R;
-  }
-  Yl[d - 1] = pack + off + slab_begin * R;
+  for (int k = 0; k < d - 1; ++k) Yl[k] = pack + poff[k];
+  Yl[d - 1] = pack + slab_off;
   KRP_CHECK_CUDA(cudaMemsetAsync(pack, 0, ysum * sizeof(float), s));
   OmegaPtrs om = make_om(omega, d, -1);
   om.p[d - 1] = omega[d - 1] + slab_begin * R;
@@ -978,12 +1002,9 @@ int krp_sketch_all_modes_dist(const float* X_slab, int d, const int64_t* dims_lo
   KRP_TRY(sketch(X_slab, g, om, R, want, Yl, ar, s));
   // one all-reduce(sum): partial Y_1..Y_{d-1} summed, zero-padded Y_d rows gathered
   KRP_TRY(allreduce_sum_f32(&comm->ctx, pack, static_cast<size_t>(ysum), s));
-  off = 0;
-  for (int k = 0; k < d; ++k) {
-    const int64_t rows = (k == d - 1) ? I_d_global : dims_local[k];
-    KRP_CHECK_CUDA(cudaMemcpyAsync(Y[k], pack + off, rows * R * sizeof(float), cudaMemcpyDeviceToDevice, s));
-    off += rows * R;
-  }
+  for (int k = 0; k < d; ++k)
+    KRP_CHECK_CUDA(cudaMemcpyAsync(Y[k], pack + poff[k], (poff[k + 1] - poff[k]) * sizeof(float),
+                                   cudaMemcpyDeviceToDevice, s));
   return KRP_OK;
 }
 

@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import dataclasses
 import math
+import os
 from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
@@ -167,14 +168,27 @@ def tensor_slab(cfg: Config, seed: int, k0: int, k1: int, parts=None, xnorm=None
     inner = int(np.prod(cfg.dims[:-1]))
     out = np.empty(inner * (k1 - k0), dtype=np.float32)
     scale = cfg.eta * xnorm / math.sqrt(cfg.N) if cfg.eta else 0.0
-    step = max(1, min(k1 - k0, (1 << 25) // max(inner, 1)))
-    for s0 in range(k0, k1, step):
-        s1 = min(k1, s0 + step)
+    step = max(1, (1 << 22) // max(inner, 1))  # chunk boundaries at global multiples of step: any slab
+                                                # request reproduces the whole tensor's bits
+
+    def fill(s0):
+        # each chunk of last-mode indices is independent (its own noise streams), so chunks are generated
+        # on a thread pool (numpy releases the GIL)
+        s1 = min(k1, (s0 // step + 1) * step)
         x0 = _x0_slab(cfg, seed, s0, s1, parts).reshape(-1, order="F")
         if scale:
             noise = np.concatenate([rng(seed, 100, kk).standard_normal(inner) for kk in range(s0, s1)])
             x0 = x0 + scale * noise
         out[(s0 - k0) * inner:(s1 - k0) * inner] = x0.astype(np.float32)
+
+    starts = [k0] + list(range((k0 // step + 1) * step, k1, step))
+    if len(starts) > 1:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=min(len(starts), os.cpu_count() or 1)) as ex:
+            list(ex.map(fill, starts))
+    else:
+        for s0 in starts:
+            fill(s0)
     return out
 
 

@@ -409,3 +409,17 @@ def test_synth_generator_recipe():
 def dataclasses_replace_eta0(cfg):
     import dataclasses
     return dataclasses.replace(cfg, eta=0.0)
+
+
+@pytest.mark.parametrize("dims", [(5, 4, 3), (3, 4, 2, 5), (2, 3, 2, 3, 2), (7, 2)])
+def test_sampled_rows_ttv_matches_explicit_kr(dims):
+    """The full-size sampled-row oracle (column identity, multi-TTV) against the explicit-KR sketch,
+    every row of every mode, on random tensors (pins sketch_rows_ttv)."""
+    g = _rng(11)
+    flat = g.standard_normal(int(np.prod(dims)))
+    om = _rand_omegas(dims, 3, 12)
+    x = oracle.as_tensor(flat, dims)
+    for n in range(len(dims)):
+        ref = oracle.sketch_mode(x, om, n)
+        got = oracle.sketch_rows_ttv(flat, dims, om, n, list(range(dims[n])))
+        assert np.allclose(got, ref, rtol=1e-12, atol=1e-12), n
