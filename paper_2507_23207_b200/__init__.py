@@ -26,7 +26,7 @@ __all__ = [
     "krp_workspace_bytes_dist", "EXPORTED_SYMBOLS", "LIB_PATH", "krp_slab_range", "krp_pack_layout",
 ]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libkrp.so")
+LIB_PATH = os.environ.get("KRP_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libkrp.so")
 OP_SKETCH_ALL, OP_SKETCH_MODE, OP_RHOSVD, OP_STHOSVD, OP_SKETCH_ALL_HOST, OP_RHOSVD_ERR = range(6)
 ENGINE_AUTO, ENGINE_TC, ENGINE_SIMT = range(3)
 

@@ -40,14 +40,12 @@ namespace krp {
 namespace {
 using namespace sm100;
 
-constexpr int kSplitPar = 1;       // split warps per TMEM lane quarter (chunk parities)
-constexpr int kNumSplitWarps = 4 * kSplitPar;
+constexpr int kNumSplitWarps = 4;  // one per TMEM lane quarter
 constexpr int kEpiWarp0 = kNumSplitWarps;
 constexpr int kNumEpiWarps = 8;    // (P | Q side) x TMEM lane quarter
 constexpr int kTmaWarp = kEpiWarp0 + kNumEpiWarps;
-constexpr int kMmaWarp = kTmaWarp + 1;   // issues the P-GEMM MMAs (and owns the TMEM allocation)
-constexpr int kMmaWarpQ = kMmaWarp + 1;  // issues the Q-GEMM MMAs
-constexpr int kThreads = (kMmaWarpQ + 1) * 32;
+constexpr int kMmaWarp = kTmaWarp + 1;  // issues every MMA and Q-view copy (and owns the TMEM allocation)
+constexpr int kThreads = (kMmaWarp + 1) * 32;
 constexpr int kTile = 128;
 constexpr int kStageFloats = 4 * 128 * 32;  // one 128x128 fp32 tile = 4 TMA boxes of {32, 128}
 constexpr int kMaxTcR = 64;
@@ -73,6 +71,7 @@ struct TcParams {
   const float* BQimg;  // [RB][NP*128]: W_L rows of row block rb
   const float* OmS;    // [S][RS]: Khatri-Rao rows of the slice modes
   long long* trace;    // development timeline (KRP_TC_TRACE): CTA 0 role timestamps, null in production
+  uint32_t wait_ns;    // mbarrier try_wait suspend-time hint (ns); 0 = spin
   int dbg;             // development bottleneck probes (KRP_TC_DEBUG): 0 normal, 1 TMA only,
                        // 2 TMA + split, 3 TMA + split + MMA (no epilogue), 4 TMA self-consumed
 };
@@ -88,6 +87,13 @@ __host__ __device__ __forceinline__ int64_t fdiv64(int64_t num, int64_t den) {
 __host__ __device__ __forceinline__ int cta_of_tile(int64_t t, int64_t T, int grid) {
   return static_cast<int>(fdiv64((t + 1) * grid - 1, T));
 }
+
+// every wait of the sketch kernel: try_wait with the plan's suspend-time hint (0 = plain spin)
+#define KWAIT(bar, par)                                              \
+  do {                                                               \
+    if (p.wait_ns) mbar_wait_hint((bar), (par), p.wait_ns);          \
+    else mbar_wait_spin((bar), (par));                               \
+  } while (0)
 
 #define KRP_TRACE(slot, idx)                                                                 \
   do {                                                                                       \
@@ -109,15 +115,79 @@ __device__ __forceinline__ void sts_f32(uint32_t saddr, float v) {
 // form), acc += z·Ω_S; on this side's T rounds, the 32-lane transposed butterfly of z·W is written to rbuf.
 // w holds this lane's Khatri-Rao row W(lane, rr..rr+8) (registers, loaded once per segment); the Ω_S row of
 // the tile is read with two 16-byte loads (rows are R8 floats, zero padded).  Adds / fmas run two-wide.
+// The two halves of a round: drain (TMEM -> z, masked) and math (acc += z·Ω_S; T butterfly).
+__device__ __forceinline__ void epi_drain8(int rnd, float (&z)[8], uint32_t tD, int R, int R8, int triple) {
+  const int rr = 8 * rnd;
+  float a[8], b[8];
+  tmem_ld8(tD + rr, a);
+  if (!triple) tmem_ld8(tD + R8 + rr, b);
+  tmem_ld_wait();
+  const bool full = rr + 8 <= R;
+#pragma unroll
+  for (int j = 0; j < 8; j += 2) {
+    float2 v = make_float2(a[j], a[j + 1]);
+    if (!triple) v = f2_add(v, make_float2(b[j], b[j + 1]));
+    if (!full) {  // columns >= R of the accumulator hold padding (possibly stale TMEM): zero them
+      v.x = rr + j < R ? v.x : 0.f;
+      v.y = rr + j + 1 < R ? v.y : 0.f;
+    }
+    z[j] = v.x;
+    z[j + 1] = v.y;
+  }
+}
+__device__ __forceinline__ void epi_math8(int rnd, const float (&z)[8], float (&acc)[8], const float* __restrict__ oms_g,
+                                          bool my_t, const float* w, uint32_t rbuf_s, int R8, uint32_t sub,
+                                          uint32_t lane) {
+  const int rr = 8 * rnd;
+  float om[8], tv[8];
+  {  // Ω_S(s, rr..rr+8): a broadcast, L1-resident global row (R8 floats, zero padded)
+    const float4 u = __ldg(reinterpret_cast<const float4*>(oms_g + rr));
+    const float4 v = __ldg(reinterpret_cast<const float4*>(oms_g + rr + 4));
+    om[0] = u.x, om[1] = u.y, om[2] = u.z, om[3] = u.w, om[4] = v.x, om[5] = v.y, om[6] = v.z, om[7] = v.w;
+  }
+#pragma unroll
+  for (int j = 0; j < 8; j += 2) {
+    const float2 zz = make_float2(z[j], z[j + 1]);
+    const float2 c = f2_fma(zz, make_float2(om[j], om[j + 1]), make_float2(acc[j], acc[j + 1]));
+    acc[j] = c.x;
+    acc[j + 1] = c.y;
+    if (my_t) {
+      const float2 t = f2_mul(zz, make_float2(w[j], w[j + 1]));
+      tv[j] = t.x;
+      tv[j + 1] = t.y;
+    }
+  }
+  if (my_t) {
+#pragma unroll
+    for (int lvl = 0; lvl < 3; ++lvl) {
+      const int m = 16 >> lvl;
+      const int h = 4 >> lvl;
+      const bool upper = (lane & m) != 0;
+#pragma unroll
+      for (int j = 0; j < h; ++j) {
+        const float send = upper ? tv[j] : tv[j + h];
+        const float keep = upper ? tv[j + h] : tv[j];
+        tv[j] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+      }
+    }
+    tv[0] += __shfl_xor_sync(0xffffffffu, tv[0], 2);
+    tv[0] += __shfl_xor_sync(0xffffffffu, tv[0], 1);
+    if ((lane & 3) == 0) sts_f32(rbuf_s + (sub * R8 + rr + (lane >> 2)) * 4, tv[0]);
+  }
+}
+
 __device__ __forceinline__ void epi_round8(int rnd, float (&acc)[8], uint32_t tD, int R, int R8, int triple,
-                                           uint32_t oms_s, bool my_t, const float* w, uint32_t rbuf_s,
+                                           const float* __restrict__ oms_g, bool my_t, const float* w, uint32_t rbuf_s,
                                            uint32_t sub, uint32_t lane) {
   const int rr = 8 * rnd;
   float a[8], b[8], om[8], tv[8];
   tmem_ld8(tD + rr, a);
   if (!triple) tmem_ld8(tD + R8 + rr, b);
-  lds_v4(oms_s + rr * 4, om[0], om[1], om[2], om[3]);
-  lds_v4(oms_s + rr * 4 + 16, om[4], om[5], om[6], om[7]);
+  {  // Ω_S(s, rr..rr+8): a broadcast, L1-resident global row (R8 floats, zero padded)
+    const float4 u = __ldg(reinterpret_cast<const float4*>(oms_g + rr));
+    const float4 v = __ldg(reinterpret_cast<const float4*>(oms_g + rr + 4));
+    om[0] = u.x, om[1] = u.y, om[2] = u.z, om[3] = u.w, om[4] = v.x, om[5] = v.y, om[6] = v.z, om[7] = v.w;
+  }
   tmem_ld_wait();
   const bool full = rr + 8 <= R;
 #pragma unroll
@@ -158,7 +228,16 @@ __device__ __forceinline__ void epi_round8(int rnd, float (&acc)[8], uint32_t tD
 }
 
 // CH: TMEM A-operand chunk width (K columns per split/MMA handshake); RA: 0 = A1/A2 accumulators in
-// TMEM, else they live in registers (RA = compile-time bound on R, a multiple of 8).
+// TMEM, else they live in registers (RA = R8, a multiple of 8).
+//
+// Synchronisation (all mbarriers; g = the CTA's running chunk index, cst = g % NC):
+//   full_x[st]      TMA landed tile stage st                          (producer tx; split + MMA warps wait)
+//   empty_x[st]     stage st may be overwritten                       (4 split arrivals + 1 MMA commit)
+//   chunk_ready[c]  chunk slot c is free: its previous MMAs are done  (1 MMA commit; split waits)
+//   chunk_full[c]   split wrote P hi / P lo / Q lo of the chunk       (4 split arrivals; MMA waits)
+//   acc_full[a]     the tile's accumulators are complete              (1 MMA commit; epilogue waits)
+//   acc_empty[a]    the epilogue drained accumulator stage a          (8 epilogue arrivals; MMA waits)
+//   b_ready         the segment's B images are in shared memory      (1 epilogue arrival; MMA waits)
 template <int CH, int RA>
 __global__ void __launch_bounds__(kThreads, 1)
     krp_tc_sketch_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ TcParams p) {
@@ -172,12 +251,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* full_x = bars;
   uint64_t* empty_x = full_x + p.NS;
   uint64_t* chunk_full = empty_x + p.NS;
-  uint64_t* chunk_empty = chunk_full + p.NC;
-  uint64_t* acc_full = chunk_empty + p.NC;
+  uint64_t* chunk_ready = chunk_full + p.NC;
+  uint64_t* acc_full = chunk_ready + p.NC;
   uint64_t* acc_empty = acc_full + p.NA;
   uint64_t* b_ready = acc_empty + p.NA;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(b_ready + 1);
-  float* wsbuf = reinterpret_cast<float*>(smem + p.sm_ws);  // [NA][RS]: Ω_S row of the tile in acc stage a
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -185,14 +263,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < p.NS; ++i) {
       mbar_init(&full_x[i], 1);
-      mbar_init(&empty_x[i], kNumSplitWarps + ((p.do_q && p.dbg != 1 && p.dbg != 4) ? 1 : 0));
+      mbar_init(&empty_x[i], kNumSplitWarps + 1);
     }
     for (int i = 0; i < p.NC; ++i) {
-      mbar_init(&chunk_full[i], 4);
-      mbar_init(&chunk_empty[i], p.do_p + p.do_q);  // one tcgen05.commit per active MMA issuer warp
+      mbar_init(&chunk_full[i], kNumSplitWarps);
+      mbar_init(&chunk_ready[i], 1);
     }
     for (int i = 0; i < p.NA; ++i) {
-      mbar_init(&acc_full[i], p.do_p + p.do_q + 1);  // the issuers' tcgen05.commits + the Ω_S bulk copy
+      mbar_init(&acc_full[i], 1);
       mbar_init(&acc_empty[i], kNumEpiWarps);
     }
     mbar_init(b_ready, 1);
@@ -206,6 +284,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * p.T / gridDim.x;
   const int64_t t1 = static_cast<int64_t>(blockIdx.x + 1) * p.T / gridDim.x;
   constexpr int nkc = kTile / CH;
+  const int64_t nchunks = (t1 - t0) * nkc;
 
   if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer
@@ -219,36 +298,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       // L2 prefetch runs kPf tiles ahead of the loads (hides DRAM hiccups behind only NS SMEM stages)
       constexpr int kPf = 3;
       int64_t pf_t = t0, pf_pair = pair, pf_s = s;
-      auto pf_advance = [&]() {
+      auto pf_issue = [&]() {
+        const int pp = static_cast<int>(pf_pair), prb = pp / p.CB, pcb = pp - prb * p.CB;  // 32-bit division
+        for (int j = 0; j < 4; ++j) tma_prefetch_3d(&tmap, prb * kTile + 32 * j, pcb * kTile, static_cast<int32_t>(pf_s));
         if (++pf_s == p.S) {
           pf_s = 0;
           ++pf_pair;
         }
         ++pf_t;
       };
-      for (int i = 0; i < kPf && pf_t < t1; ++i) {
-        const int prb = static_cast<int>(pf_pair / p.CB), pcb = static_cast<int>(pf_pair % p.CB);
-        for (int j = 0; j < 4; ++j) tma_prefetch_3d(&tmap, prb * kTile + 32 * j, pcb * kTile, static_cast<int32_t>(pf_s));
-        pf_advance();
-      }
+      for (int i = 0; i < kPf && pf_t < t1; ++i) pf_issue();
       for (int64_t t = t0; t < t1; ++t) {
-        if (pf_t < t1) {
-          const int prb = static_cast<int>(pf_pair / p.CB), pcb = static_cast<int>(pf_pair % p.CB);
-          for (int j = 0; j < 4; ++j)
-            tma_prefetch_3d(&tmap, prb * kTile + 32 * j, pcb * kTile, static_cast<int32_t>(pf_s));
-          pf_advance();
-        }
-        if (p.dbg == 4) {  // probe: the producer consumes its own stages (no handshake)
-          if (t - t0 >= p.NS) mbar_wait(&full_x[st], ph ^ 1);
-        } else {
-          mbar_wait(&empty_x[st], ph ^ 1);
-        }
+        if (pf_t < t1) pf_issue();
+        KWAIT(&empty_x[st], ph ^ 1);
         KRP_TRACE(0, t - t0);
         mbar_arrive_expect_tx(&full_x[st], kStageFloats * 4);
         float* dst = xs + st * kStageFloats;
         for (int j = 0; j < 4; ++j)
-          tma_load_3d(dst + j * 4096, &tmap, &full_x[st], rb * kTile + 32 * j, cb * kTile, static_cast<int32_t>(s),
-                      pol);
+          tma_load_3d(dst + j * 4096, &tmap, &full_x[st], rb * kTile + 32 * j, cb * kTile, static_cast<int32_t>(s), pol);
         if (++st == p.NS) {
           st = 0;
           ph ^= 1;
@@ -260,183 +327,141 @@ __global__ void __launch_bounds__(kThreads, 1)
           cb = static_cast<int>(pair % p.CB);
         }
       }
-      if (p.dbg == 4) {  // drain the stages still in flight
-        for (int64_t t = (t1 - p.NS > t0 ? t1 - p.NS : t0); t < t1; ++t) {
-          const int s2 = static_cast<int>((t - t0) % p.NS);
-          mbar_wait(&full_x[s2], static_cast<uint32_t>(((t - t0) / p.NS) & 1));
-        }
-      }
     }
-  } else if (warp == kMmaWarp || warp == kMmaWarpQ) {
-    // ------------------------------------------------------------ MMA issuers: one warp per GEMM
-    // The whole warp runs the loop (so every address / descriptor is warp-uniform and lives in uniform
-    // registers); one elected lane issues the tcgen05 instructions.  Descriptors are formed once and
-    // advanced by adding (byte offset >> 4) to the start-address field.
-    const bool qgemm = (warp == kMmaWarpQ);
-    if (qgemm ? p.do_q : p.do_p) {
-      const bool leader = elect_one();
-      const uint32_t idesc1 = make_idesc_tf32(128, p.NP, 0, 0);
-      const uint32_t idesc2 = make_idesc_tf32(128, p.N2, 0, 0);
-      const uint64_t bdesc0 = make_smem_desc(smem_u32(qgemm ? bq : bp), 0, 1024, kLayoutSW128);
-      const uint64_t adesc0 = make_smem_desc(smem_u32(xs), 0, 1024, kLayoutSW128);
-      const uint64_t lo_d = static_cast<uint64_t>(p.R8) * 8;        // B_lo rows start at R8: (R8*128 B) >> 4
-      const uint64_t katom_d = static_cast<uint64_t>(p.NP) * 8;     // one 32-wide K atom of B: (NP*128 B) >> 4
-      int cst = 0, ast = 0, xst = 0;
-      uint32_t cph = 0, aph = 0, bph = 0;
-      int64_t s_cur = t0 % p.S;
-      bool first = true;
-      for (int64_t t = t0; t < ((p.dbg == 1 || p.dbg == 4) ? t0 : t1); ++t) {
-        if (first || s_cur == 0) {  // a new (row block, col block) segment: wait for its B operands
-          mbar_wait(b_ready, bph);
-          bph ^= 1;
-          first = false;
-        }
-        if (p.dbg == 0 || p.dbg == 5 || p.dbg >= 7) mbar_wait(&acc_empty[ast], aph ^ 1);
-        if (leader) KRP_TRACE(3, t - t0);
-        tc_fence_after();
-        if (qgemm == !p.do_p && leader) {  // Ω_S(s, :) for the epilogue, on the same barrier as the accumulator
-          mbar_arrive_expect_tx(&acc_full[ast], p.RS * 4);
-          bulk_copy_g2s(wsbuf + ast * p.RS, p.OmS + s_cur * p.RS, p.RS * 4, &acc_full[ast]);
-        }
-        const uint32_t dacc = tbase + p.tm_acc + ast * 2 * p.DN + (qgemm ? p.DN : 0);
+  } else if (warp == kMmaWarp) {
+    // ------------------------------------------------------------ MMA issuer (both GEMMs)
+    // The whole warp runs the loop (warp-uniform descriptors in uniform registers); one elected lane
+    // issues.  Descriptors advance by (byte offset >> 4) on the start-address field.
+    const bool leader = elect_one();
+    const uint32_t idesc1 = make_idesc_tf32(128, p.NP, 0, 0);
+    const uint32_t idesc2 = make_idesc_tf32(128, p.N2, 0, 0);
+    const uint64_t bpdesc0 = make_smem_desc(smem_u32(bp), 0, 1024, kLayoutSW128);
+    const uint64_t bqdesc0 = make_smem_desc(smem_u32(bq), 0, 1024, kLayoutSW128);
+    const uint64_t adesc0 = make_smem_desc(smem_u32(xs), 0, 1024, kLayoutSW128);
+    const uint64_t lo_d = static_cast<uint64_t>(p.R8) * 8;     // B_lo rows start at R8: (R8*128 B) >> 4
+    const uint64_t katom_d = static_cast<uint64_t>(p.NP) * 8;  // one 32-wide K atom of B: (NP*128 B) >> 4
+    int ast = 0, xst = 0, cst = 0;
+    uint32_t aph = 0, bph = 0, cph = 0;
+    int64_t s_cur = t0 % p.S;
+    bool first = true;
+    for (int64_t t = t0; t < t1; ++t) {
+      if (first || s_cur == 0) {  // a new (row block, col block) segment: wait for its B operands
+        KWAIT(b_ready, bph);
+        bph ^= 1;
+        first = false;
+      }
+      KWAIT(&acc_empty[ast], aph ^ 1);
+      if (leader) KRP_TRACE(3, t - t0);
+      tc_fence_after();
+      const uint32_t dP = tbase + p.tm_acc + ast * 2 * p.DN;
+      const uint32_t dQ = dP + p.DN;
         const uint64_t adesc_t = adesc0 + ((static_cast<uint64_t>(xst) * (kStageFloats * 4)) >> 4);
-        for (int kc = 0; kc < nkc; ++kc) {
-          mbar_wait(&chunk_full[cst], cph);
-          if (leader) KRP_TRACE(10 + (qgemm ? 2 : 0), (t - t0) * 8 + kc);
-          tc_fence_after();
-          // A chunk in TMEM: P uses [hi | lo] at ch, ch + CH; Q uses lo at ch + 2 CH (hi from SMEM)
-          const uint32_t ach = tbase + p.tm_chunk + cst * 3 * CH + (qgemm ? 2 * CH : 0);
-          // first K-step of the chunk: kk0 = kc*CH/8; B atom kk0>>2, offset (kk0&3)*32 B
-          const int kk0 = kc * (CH / 8);
-          const uint64_t bchunk = bdesc0 + static_cast<uint64_t>(kk0 >> 2) * katom_d + (kk0 & 3) * 2;
-          const uint64_t achunk = adesc_t + static_cast<uint64_t>(kk0 >> 2) * 1024 + (kk0 & 3) * 2;  // 16 KB boxes
-          if (p.dbg != 2 && leader) {
-            if (p.triple) {
+      for (int kc = 0; kc < nkc; ++kc) {
+        KWAIT(&chunk_full[cst], cph);
+        if (leader) KRP_TRACE(10, (t - t0) * 8 + kc);
+        tc_fence_after();
+        const uint32_t ach = tbase + p.tm_chunk + cst * 3 * CH;  // [P hi | P lo | Q lo]
+        const int kk0 = kc * (CH / 8);
+        const uint64_t boff = static_cast<uint64_t>(kk0 >> 2) * katom_d + (kk0 & 3) * 2;
+        // Q's A_hi: the raw tile in stage xst, box kk0/4 (16 KB), K offset (kk0 & 3) * 32 B
+        const uint64_t aq = adesc_t + static_cast<uint64_t>(kk0 >> 2) * 1024 + (kk0 & 3) * 2;
+        if (leader) {
+          if (p.triple) {
 #pragma unroll
-              for (int ks = 0; ks < CH / 8; ++ks) {
-                const uint64_t bd = bchunk + ks * 2, bl = bd + lo_d;
-                const uint32_t acc0 = (kk0 + ks) > 0 ? 1u : 0u;
-                if (!qgemm) {
-                  mma_tf32_ts(dacc, ach + 8 * ks, bd, idesc2, acc0);       // hi x hi
-                  mma_tf32_ts(dacc, ach + 8 * ks, bl, idesc2, 1u);         // hi x lo
-                  mma_tf32_ts(dacc, ach + CH + 8 * ks, bd, idesc2, 1u);    // lo x hi
-                } else {
-                  const uint64_t ad = achunk + ks * 2;
-                  mma_tf32_ss(dacc, ad, bd, idesc2, acc0);
-                  mma_tf32_ss(dacc, ad, bl, idesc2, 1u);
-                  mma_tf32_ts(dacc, ach + 8 * ks, bd, idesc2, 1u);
-                }
-              }
-            } else {
-#pragma unroll
-              for (int ks = 0; ks < CH / 8; ++ks) {
-                const uint64_t bd = bchunk + ks * 2;
-                const uint32_t acc0 = (kk0 + ks) > 0 ? 1u : 0u;
-                if (!qgemm) {
-                  mma_tf32_ts(dacc, ach + 8 * ks, bd, idesc1, acc0);       // hi x [B_hi | B_lo]
-                  mma_tf32_ts(dacc, ach + CH + 8 * ks, bd, idesc2, 1u);    // lo x B_hi
-                } else {
-                  // A_hi = the raw fp32 tile straight from shared memory (K-major: K = ρ along the 128 B
-                  // rows of box kk/4, M = γ rows, SWIZZLE_128B, 8-row atoms 1 KB apart); the tensor core
-                  // reads it truncated to tf32, i.e. exactly hi.
-                  mma_tf32_ss(dacc, achunk + ks * 2, bd, idesc1, acc0);
-                  mma_tf32_ts(dacc, ach + 8 * ks, bd, idesc2, 1u);
-                }
-              }
+            for (int ks = 0; ks < CH / 8; ++ks) {
+              const uint32_t acc0 = (kk0 + ks) > 0 ? 1u : 0u;
+              const uint64_t bd = bpdesc0 + boff + ks * 2, bdq = bqdesc0 + boff + ks * 2;
+              mma_tf32_ts(dP, ach + 8 * ks, bd, idesc2, acc0);              // P: hi x hi
+              mma_tf32_ts(dP, ach + 8 * ks, bd + lo_d, idesc2, 1u);         //    hi x lo
+              mma_tf32_ts(dP, ach + CH + 8 * ks, bd, idesc2, 1u);           //    lo x hi
+              mma_tf32_ss(dQ, aq + ks * 2, bdq, idesc2, acc0);              // Q: hi (SMEM) x hi
+              mma_tf32_ss(dQ, aq + ks * 2, bdq + lo_d, idesc2, 1u);         //    hi x lo
+              mma_tf32_ts(dQ, ach + 2 * CH + 8 * ks, bdq, idesc2, 1u);      //    lo x hi
             }
-          }
-          if (leader) {
-            mma_commit(&chunk_empty[cst]);
-            KRP_TRACE(11 + (qgemm ? 2 : 0), (t - t0) * 8 + kc);
-          }
-          __syncwarp();
-          if (++cst == p.NC) {
-            cst = 0;
-            cph ^= 1;
+          } else {
+#pragma unroll
+            for (int ks = 0; ks < CH / 8; ++ks) {
+              const uint32_t acc0 = (kk0 + ks) > 0 ? 1u : 0u;
+              const uint64_t bd = bpdesc0 + boff + ks * 2, bdq = bqdesc0 + boff + ks * 2;
+              mma_tf32_ts(dP, ach + 8 * ks, bd, idesc1, acc0);              // P: hi x [B_hi | B_lo]
+              mma_tf32_ts(dP, ach + CH + 8 * ks, bd, idesc2, 1u);           //    lo x B_hi
+              mma_tf32_ss(dQ, aq + ks * 2, bdq, idesc1, acc0);              // Q: hi (SMEM) x [B_hi | B_lo]
+              mma_tf32_ts(dQ, ach + 2 * CH + 8 * ks, bdq, idesc2, 1u);      //    lo x B_hi
+            }
           }
         }
         if (leader) {
-          if (qgemm) mma_commit(&empty_x[xst]);  // the raw tile may be overwritten once these MMAs finish
-          mma_commit(&acc_full[ast]);
-          KRP_TRACE(4, t - t0);
+          mma_commit(&chunk_ready[cst]);  // the slot is free again once these MMAs finish
+          KRP_TRACE(11, (t - t0) * 8 + kc);
         }
         __syncwarp();
-        if (++xst == p.NS) xst = 0;
-        if (++ast == p.NA) {
-          ast = 0;
-          aph ^= 1;
-        }
-        if (++s_cur == p.S) s_cur = 0;
-      }
-    }
-  } else if (warp < kNumSplitWarps) {
-    // ------------------------------------------------------------ split warps: SMEM tile -> TMEM hi/lo
-    // warp w stages the chunks kc with kc % 2 == w / 4 of every tile, for TMEM lane quarter w % 4
-    const uint32_t sub = warp & 3;
-    const int par = static_cast<int>(warp >> 2);  // chunk parity handled by this warp (kSplitPar == 2)
-    const uint32_t lane_off = (32u * sub) << 16;
-    int xst = 0;
-    uint32_t xph = 0;
-    int cst = 0;  // chunk stage / phase of the chunk being processed (every chunk, both parities)
-    uint32_t cph = 0;
-    const bool dop = p.do_p && p.dbg != 5 && p.dbg != 6, doq = p.do_q && p.dbg != 5 && p.dbg != 6;
-    const int gq = static_cast<int>(32 * sub + lane);
-    // Shared-window addresses with the SWIZZLE_128B pattern folded in, so every load below is
-    // register + immediate.  P view: element (ρ = 32*sub + lane, γ) of box `sub` sits at byte
-    // γ*128 + (((lane>>2) ^ (γ&7)) << 4) + (lane&3)*4; γ&7 is a compile-time j&7 in the loop.
-    uint32_t psw[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      psw[j] = smem_u32(xs) + sub * 16384u + ((((lane >> 2) ^ static_cast<uint32_t>(j)) << 4) | ((lane & 3u) << 2));
-    // Q view: row γ = gq of box b holds ρ = 32b..32b+31; 16-byte chunk c of it sits at ((c ^ (gq&7)) << 4)
-    const uint32_t qrow = smem_u32(xs) + static_cast<uint32_t>(gq) * 128u;
-    const uint32_t qx = static_cast<uint32_t>(gq & 7);
-    for (int64_t t = t0; t < t1; ++t) {
-      mbar_wait(&full_x[xst], xph);
-      if (sub == 0 && par == 0 && lane == 0) KRP_TRACE(1, t - t0);
-      const float* X = xs + xst * kStageFloats;
-      if (p.dbg == 4) break;
-      for (int kc = 0; kc < (p.dbg == 1 ? 0 : nkc); ++kc) {
-        const int my_cst = cst;
-        const uint32_t my_cph = cph;
         if (++cst == p.NC) {
           cst = 0;
           cph ^= 1;
         }
-        if (kSplitPar == 2 && (kc & 1) != par) continue;
-        mbar_wait(&chunk_empty[my_cst], my_cph ^ 1);
+      }
+      if (leader) {
+        mma_commit(&empty_x[xst]);  // the raw tile (Q's A_hi) may be overwritten once these MMAs finish
+        mma_commit(&acc_full[ast]);
+        KRP_TRACE(4, t - t0);
+      }
+      __syncwarp();
+      if (++xst == p.NS) xst = 0;
+      if (++ast == p.NA) {
+        ast = 0;
+        aph ^= 1;
+      }
+      if (++s_cur == p.S) s_cur = 0;
+    }
+  } else if (warp < kNumSplitWarps) {
+    // ------------------------------------------------------------ split warps: tile -> TMEM hi / lo
+    // P view (lane = ρ): shared-memory loads (the transpose), hi = raw value, lo = x - tf32(x).
+    // Q view (lane = γ): 16-byte loads of the rows; only lo goes to TMEM (Q's hi is read from SMEM).
+    const uint32_t sub = warp & 3;
+    const uint32_t lane_off = (32u * sub) << 16;
+    int xst = 0;
+    uint32_t xph = 0;
+    const bool dop = p.do_p != 0, doq = p.do_q != 0;
+    // P view: element (ρ = 32*sub + lane, γ) of box `sub` sits at byte γ*128 + (((lane>>2) ^ (γ&7)) << 4) +
+    // (lane&3)*4; γ&7 is the compile-time j&7 below, so every load is register + immediate.
+    uint32_t psw[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      psw[j] = smem_u32(xs) + sub * 16384u + ((((lane >> 2) ^ static_cast<uint32_t>(j)) << 4) | ((lane & 3u) << 2));
+    const uint32_t gq = 32 * sub + lane;
+    const uint32_t qrow = smem_u32(xs) + gq * 128u, qx = gq & 7u;
+    int cst = 0;
+    uint32_t cph = 0;
+    for (int64_t t = t0; t < t1; ++t) {
+      KWAIT(&full_x[xst], xph);
+      if (sub == 0 && lane == 0) KRP_TRACE(1, t - t0);
+      const uint32_t stage_off = static_cast<uint32_t>(xst) * (kStageFloats * 4u);
+      for (int kc = 0; kc < nkc; ++kc) {
+        KWAIT(&chunk_ready[cst], cph ^ 1);
         if (sub == 0 && lane == 0) KRP_TRACE(8, (t - t0) * 8 + kc);
         tc_fence_after();
-        const uint32_t ch = tbase + lane_off + p.tm_chunk + my_cst * 3 * CH;
-        const uint32_t stage_off = static_cast<uint32_t>(xst) * (kStageFloats * 4u);
-        // All shared-memory loads of the chunk are issued first (one load latency per chunk, not one per
-        // 16 columns), then hi / lo are formed and stored to TMEM with one 32x32b.xCH store each.
-        uint32_t px[CH];
-        float qv[CH];
-        if (dop && p.dbg == 8) {
-#pragma unroll
-          for (int j = 0; j < CH; ++j) px[j] = __float_as_uint(1.0f + j);
-        }
-        if (dop && p.dbg != 8) {
-          // lane = ρ = 32*sub + lane (box `sub`), columns γ = kc*CH + j (rows of the box)
+        const uint32_t ch = tbase + lane_off + p.tm_chunk + cst * 3 * CH;
+        // all shared-memory loads of the chunk first (one load latency per chunk)
+        uint32_t px[CH], qv[CH];
+        if (dop) {
           const uint32_t goff = stage_off + static_cast<uint32_t>(kc * CH) * 128u;
 #pragma unroll
           for (int j = 0; j < CH; ++j) px[j] = __float_as_uint(lds_f32(psw[j & 7] + goff + static_cast<uint32_t>(j) * 128u));
         }
-        if (doq && p.dbg == 7) {
-#pragma unroll
-          for (int j = 0; j < CH; ++j) qv[j] = 1.0f + j;
-        }
-        if (doq && p.dbg != 7) {
-          // lane = γ = 32*sub + lane, columns ρ = kc*CH + j: CH consecutive ρ of row γ (16-byte chunks)
+        if (doq) {
+          // lane = γ, columns ρ = kc*CH + j: CH consecutive ρ of row γ (16-byte chunks, swizzled)
           const int rho0 = kc * CH;
           const uint32_t rowa = qrow + stage_off + static_cast<uint32_t>(rho0 >> 5) * 16384u;
 #pragma unroll
           for (int qq = 0; qq < CH / 4; ++qq) {
             const uint32_t chunk = ((static_cast<uint32_t>(rho0 & 31) >> 2) + qq) ^ qx;
-            lds_v4(rowa + (chunk << 4), qv[4 * qq], qv[4 * qq + 1], qv[4 * qq + 2], qv[4 * qq + 3]);
+            float a0, a1, a2, a3;
+            lds_v4(rowa + (chunk << 4), a0, a1, a2, a3);
+            qv[4 * qq] = __float_as_uint(a0), qv[4 * qq + 1] = __float_as_uint(a1);
+            qv[4 * qq + 2] = __float_as_uint(a2), qv[4 * qq + 3] = __float_as_uint(a3);
           }
         }
+        if (sub == 0 && lane == 0) KRP_TRACE(14, (t - t0) * 8 + kc);
         if (dop) {
           tmem_st<CH>(ch + 0 * CH, px);  // hi: the raw value (the tensor core truncates to tf32)
           uint32_t lo[CH];
@@ -450,24 +475,28 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st<CH>(ch + 1 * CH, lo);
         }
         if (doq) {
-          uint32_t lo[CH];
 #pragma unroll
           for (int j = 0; j < CH; j += 2) {
-            const float2 l = f2_sub(make_float2(qv[j], qv[j + 1]),
-                                    make_float2(__uint_as_float(tf32_hi_bits(qv[j])), __uint_as_float(tf32_hi_bits(qv[j + 1]))));
-            lo[j] = __float_as_uint(l.x);
-            lo[j + 1] = __float_as_uint(l.y);
+            const float2 x = make_float2(__uint_as_float(qv[j]), __uint_as_float(qv[j + 1]));
+            const float2 l = f2_sub(x, make_float2(__uint_as_float(tf32_hi_bits(x.x)), __uint_as_float(tf32_hi_bits(x.y))));
+            qv[j] = __float_as_uint(l.x);
+            qv[j + 1] = __float_as_uint(l.y);
           }
-          tmem_st<CH>(ch + 2 * CH, lo);
+          tmem_st<CH>(ch + 2 * CH, qv);  // Q lo
         }
+        if (sub == 0 && lane == 0) KRP_TRACE(15, (t - t0) * 8 + kc);
         tmem_st_wait();
         if (sub == 0 && lane == 0) KRP_TRACE(9, (t - t0) * 8 + kc);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&chunk_full[my_cst]);
+        if (lane == 0) mbar_arrive(&chunk_full[cst]);
+        if (++cst == p.NC) {
+          cst = 0;
+          cph ^= 1;
+        }
       }
       __syncwarp();
-      if (sub == 0 && par == 0 && lane == 0) KRP_TRACE(2, t - t0);
+      if (sub == 0 && lane == 0) KRP_TRACE(2, t - t0);
       if (lane == 0) mbar_arrive(&empty_x[xst]);
       if (++xst == p.NS) {
         xst = 0;
@@ -572,27 +601,26 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (p.dbg != 0 && p.dbg != 5 && p.dbg < 7) continue;
-      mbar_wait(&acc_full[ast], aph);
+      KWAIT(&acc_full[ast], aph);
       if (ew == 0 && lane == 0) KRP_TRACE(5, t - t0);
       tc_fence_after();
       const uint32_t tD = tbase + lane_off + p.tm_acc + ast * 2 * p.DN + (pside ? 0 : p.DN);
-      const uint32_t oms_s = smem_u32(wsbuf + ast * p.RS);
+      const float* oms_g = p.OmS + s * p.RS;
       const uint32_t rbuf_s = smem_u32(red + parity * (4 * R8));
       float* rbuf = red + parity * (4 * R8);
+      bool released = false;
       if (active) {
         if constexpr (RA > 0) {
 #pragma unroll
           for (int rnd = 0; rnd < RA / 8; ++rnd) {
-            if (8 * rnd < R) {
-              float acc8[8];  // register copies (no pointer into Areg, which must stay in registers)
+            float acc8[8], z8[8];  // register copies (no pointer into Areg, which must stay in registers)
+            epi_drain8(rnd, z8, tD, R, R8, p.triple);
 #pragma unroll
-              for (int j = 0; j < 8; ++j) acc8[j] = Areg[8 * rnd + j];
-              epi_round8(rnd, acc8, tD, R, R8, p.triple, oms_s, p.do_t && ((rnd & 1) == (pside ? 0 : 1)),
-                         &wreg[8 * (rnd >> 1)], rbuf_s, sub, lane);
+            for (int j = 0; j < 8; ++j) acc8[j] = Areg[8 * rnd + j];
+            epi_math8(rnd, z8, acc8, oms_g, p.do_t && ((rnd & 1) == (pside ? 0 : 1)), &wreg[8 * (rnd >> 1)], rbuf_s,
+                      R8, sub, lane);
 #pragma unroll
-              for (int j = 0; j < 8; ++j) Areg[8 * rnd + j] = acc8[j];
-            }
+            for (int j = 0; j < 8; ++j) Areg[8 * rnd + j] = acc8[j];
           }
         } else {
 #pragma unroll
@@ -600,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (rnd < nr) {
               float acc[8];
               tmem_ld8(tA + 8 * rnd, acc);
-              epi_round8(rnd, acc, tD, R, R8, p.triple, oms_s, p.do_t && ((rnd & 1) == (pside ? 0 : 1)),
+              epi_round8(rnd, acc, tD, R, R8, p.triple, oms_g, p.do_t && ((rnd & 1) == (pside ? 0 : 1)),
                          &wreg[8 * (rnd >> 1)], rbuf_s, sub, lane);
               uint32_t accb[8];
 #pragma unroll
@@ -611,10 +639,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st_wait();
         }
       }
-      // every TMEM read of this tile is done: hand the accumulator stage back to the MMA warp
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[ast]);
+      if (!released) {  // every TMEM access of this tile is done: hand the accumulator stage back
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[ast]);
+      }
       if (++ast == p.NA) {
         ast = 0;
         aph ^= 1;
@@ -962,7 +991,7 @@ bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, TcPlan& pl
   {
     struct Opt {
       int triple, na, ch, ncmin, areg;
-    } opts[8] = {{0, 2, 16, 4, 1}, {0, 2, 32, 2, 1}, {1, 2, 32, 2, 1}, {0, 2, 32, 2, 0},
+    } opts[8] = {{0, 2, 32, 2, 1}, {0, 2, 16, 4, 1}, {1, 2, 32, 2, 1}, {0, 2, 32, 2, 0},
                  {0, 2, 16, 3, 0}, {1, 2, 32, 2, 0}, {1, 2, 16, 2, 0}, {1, 1, 16, 2, 0}};
     pl.NC = 0;
     const char* force = getenv("KRP_TC_OPT");  // development: force one option (if it fits)
@@ -984,7 +1013,7 @@ bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, TcPlan& pl
         break;
       }
     }
-    if (pl.NC < 2) return false;
+    if (pl.NC < 2 || pl.NC > kTile / pl.CH) return false;  // copies run at most one tile ahead
     pl.NP = pl.triple ? pl.R8 + pl.N2 : pl.DN;  // B-image rows (hi rows [0,R), lo rows [R8, R8+R))
   }
   pl.tm_acc = 0;
@@ -1170,6 +1199,8 @@ int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const b
   {
     const char* e = getenv("KRP_TC_DEBUG");
     p.dbg = e ? atoi(e) : 0;
+    const char* w = getenv("KRP_TC_WAIT_NS");
+    p.wait_ns = w ? static_cast<uint32_t>(atol(w)) : 10000000u;
     p.trace = nullptr;
     if (getenv("KRP_TC_TRACE")) {
       static long long* tr = nullptr;

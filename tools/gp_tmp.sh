@@ -1,4 +1,6 @@
-mkdir -p gpurun_out/r01q
-timeout 1500 python -m pytest tests -m gpu -x -q -rs --durations=15 > gpurun_out/r01q/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r01q/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r01q/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/r01q/smoke.log
-free -g > gpurun_out/r01q/mem.txt; nproc >> gpurun_out/r01q/mem.txt
+mkdir -p gpurun_out/ab3
+timeout 300 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/ab3/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/ab3/pytest_gpu.log
+for c in c2 c3 c4 c5; do
+ echo "old"; KRP_LIB=$PWD/abtest/libkrp_old.so KRP_TC_OPT=1 timeout 60 python tools/tc_time.py $c 20
+ echo "new"; timeout 60 python tools/tc_time.py $c 20
+done > gpurun_out/ab3/time.log 2>&1

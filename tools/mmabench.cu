@@ -16,6 +16,7 @@ using namespace sm100;
 
 struct alignas(1024) Smem {
   float a[4][128][32];  // 64 KB tile, 4 boxes {32 K, 128 rows}, SW128 K-major
+  float land[2][4096];  // 2 x 16 KB landing buffers for the background bulk copies (BG variants)
   float b[2][4][96][32];  // two B images (P, Q): 4 K atoms x up to 96 rows x 32
   uint64_t bar[8];
   uint32_t tbase;
@@ -23,13 +24,16 @@ struct alignas(1024) Smem {
 
 // VAR: 0 = one issuer, Q-hi SS; 1 = one issuer, Q-hi TS; 2 = two issuers (P / Q warps), Q-hi SS;
 //      3 = P only (TS); 4 = Q only (SS hi); 5 = one issuer, all TS, N=NC only (no lo x hi)
-template <int VAR, int NCAT, int NLO>
-__global__ void __launch_bounds__(128, 1) mma_kernel(int chunks, unsigned long long* out) {
+template <int VAR, int NCAT, int NLO, int BG = 0, int RND = 0>
+__global__ void __launch_bounds__(128, 1) mma_kernel(int chunks, unsigned long long* out, const float* gsrc = nullptr,
+                                                     volatile int* stop = nullptr) {
   extern __shared__ __align__(1024) uint8_t raw[];
   Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
   const uint32_t warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < 4 * 128 * 32; i += 128) (&s.a[0][0][0])[i] = 1.0f;
-  for (int i = threadIdx.x; i < 2 * 4 * 96 * 32; i += 128) (&s.b[0][0][0][0])[i] = 0.5f;
+  for (int i = threadIdx.x; i < 4 * 128 * 32; i += 128)
+    (&s.a[0][0][0])[i] = RND ? __uint_as_float(0x3f800000u | ((i * 2654435761u) >> 9)) * ((i & 1) ? 1.f : -1.f) : 1.0f;
+  for (int i = threadIdx.x; i < 2 * 4 * 96 * 32; i += 128)
+    (&s.b[0][0][0][0])[i] = RND ? __uint_as_float(0x3f000000u | ((i * 40503u * 2654435761u) >> 9)) * ((i & 2) ? 1.f : -1.f) : 0.5f;
   if (warp == 0) tmem_alloc<512>(&s.tbase);
   if (threadIdx.x == 0) {
     for (int i = 0; i < 8; ++i) mbar_init(&s.bar[i], VAR == 2 ? 2 : 1);
@@ -46,6 +50,28 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int chunks, unsigned long l
   const uint64_t a0 = make_smem_desc(smem_u32(&s.a[0][0][0]), 0, 1024, kLayoutSW128);
   const uint64_t katom = 96 * 8;
   const bool issuer = (VAR == 2) ? (warp < 2) : (warp == 0);
+  if (BG && warp == 3) {  // background producer: 16 KB bulk copies global -> SMEM, as fast as they land
+    if (elect_one()) {
+      __shared__ uint64_t lb[2];
+      mbar_init(&lb[0], 1);
+      mbar_init(&lb[1], 1);
+      fence_barrier_init();
+      uint32_t ph[2] = {0, 0};
+      for (int i = 0; i < 2; ++i) {
+        mbar_arrive_expect_tx(&lb[i], 16384);
+        bulk_copy_g2s(&s.land[i][0], gsrc + (size_t)(blockIdx.x * 64 + i) * 4096, 16384, &lb[i]);
+      }
+      for (int i = 2; i < chunks * 3 / 4 + 2; ++i) {  // ~ 12 KB per chunk (64 KB per 4 chunks + margin)
+        const int b = i & 1;
+        mbar_wait(&lb[b], ph[b]);
+        ph[b] ^= 1;
+        mbar_arrive_expect_tx(&lb[b], 16384);
+        bulk_copy_g2s(&s.land[b][0], gsrc + ((size_t)(blockIdx.x * 997 + i) % 65536) * 4096, 16384, &lb[b]);
+      }
+      mbar_wait(&lb[0], ph[0]);
+      mbar_wait(&lb[1], ph[1]);
+    }
+  }
   long long t0 = clock64();
   if (issuer && elect_one()) {
     const bool doP = VAR != 4 && !(VAR == 2 && warp == 1);
@@ -85,20 +111,22 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int chunks, unsigned long l
   if (warp == 0) tmem_dealloc<512>(tb);
 }
 
-template <int VAR, int NCAT, int NLO>
+template <int VAR, int NCAT, int NLO, int BG = 0, int RND = 0>
 void run(const char* name) {
   const int nsm = 148, chunks = 20000;
-  auto k = mma_kernel<VAR, NCAT, NLO>;
+  auto k = mma_kernel<VAR, NCAT, NLO, BG, RND>;
+  static float* gsrc = nullptr;
+  if (!gsrc) cudaMalloc(&gsrc, (size_t)65536 * 4096 * 4);  // 1 GiB source for the background copies
   const size_t smem = sizeof(Smem) + 1024;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   unsigned long long* d;
   cudaMalloc(&d, nsm * 8);
-  k<<<nsm, 128, smem>>>(100, d);
+  k<<<nsm, 128, smem>>>(100, d, gsrc, nullptr);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  k<<<nsm, 128, smem>>>(chunks, d);
+  k<<<nsm, 128, smem>>>(chunks, d, gsrc, nullptr);
   cudaEventRecord(e1);
   cudaError_t e = cudaDeviceSynchronize();
   float ms;
@@ -113,14 +141,10 @@ void run(const char* name) {
 }
 
 int main() {
-  run<0, 80, 48>("1 issuer, P TS + Q SS-hi (kernel mix R=40)");
-  run<1, 80, 48>("1 issuer, P TS + Q TS-hi");
-  run<2, 80, 48>("2 issuers (P warp, Q warp), Q SS-hi");
-  run<3, 80, 48>("P only (TS)");
-  run<4, 80, 48>("Q only (SS hi + TS lo)");
-  run<5, 80, 48>("hi x [Bhi|Blo] only, both TS");
-  run<0, 64, 32>("1 issuer, kernel mix R=30");
-  run<0, 48, 32>("1 issuer, kernel mix R=20");
-  run<0, 128, 64>("1 issuer, kernel mix R=60");
+  run<2, 80, 48>("2 issuers, Q SS-hi, constant data");
+  run<2, 80, 48, 0, 1>("2 issuers, Q SS-hi, random data");
+  run<1, 80, 48>("1 issuer, Q TS-hi, constant data");
+  run<1, 80, 48, 0, 1>("1 issuer, Q TS-hi, random data");
+  run<3, 80, 48, 0, 1>("P only, random data");
   return 0;
 }

@@ -19,17 +19,42 @@ __device__ __forceinline__ float lds_f32(uint32_t a) {
 }
 __device__ __forceinline__ uint32_t hib(float x) { return __float_as_uint(x) & 0xFFFFE000u; }
 
-template <int VAR>
-__global__ void __launch_bounds__(128, 1) split_kernel(int iters, unsigned long long* out, float* sink) {
+template <int VAR, int BG = 0>
+__global__ void __launch_bounds__(160, 1) split_kernel(int iters, unsigned long long* out, float* sink,
+                                                       const float* gsrc) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t tb_s;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* xs = reinterpret_cast<float*>(smem);
   for (int i = threadIdx.x; i < 16384; i += 128) xs[i] = 1.0f + i * 1e-3f;
+  __shared__ uint64_t lb[2];
   if (warp == 0) tmem_alloc<512>(&tb_s);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (warp == 4) {  // background bulk copies into a second 64 KB region (TMA-like SMEM writes)
+    if (BG && elect_one()) {
+      float* land = xs + 16384;
+      mbar_init(&lb[0], 1);
+      mbar_init(&lb[1], 1);
+      fence_barrier_init();
+      uint32_t ph[2] = {0, 0};
+      for (int i = 0; i < 2; ++i) {
+        mbar_arrive_expect_tx(&lb[i], 32768);
+        bulk_copy_g2s(land + i * 8192, gsrc + (size_t)(blockIdx.x * 64 + i) * 8192, 32768, &lb[i]);
+      }
+      for (int i = 2; i < iters * 2; ++i) {
+        const int b = i & 1;
+        mbar_wait(&lb[b], ph[b]);
+        ph[b] ^= 1;
+        mbar_arrive_expect_tx(&lb[b], 32768);
+        bulk_copy_g2s(land + b * 8192, gsrc + ((size_t)(blockIdx.x * 997 + i) % 32768) * 8192, 32768, &lb[b]);
+      }
+      mbar_wait(&lb[0], ph[0]);
+      mbar_wait(&lb[1], ph[1]);
+    }
+    return;
+  }
   const uint32_t sub = warp;
   const uint32_t ch0 = tb_s + ((32u * sub) << 16);
   uint32_t psw[8];
@@ -82,20 +107,22 @@ __global__ void __launch_bounds__(128, 1) split_kernel(int iters, unsigned long 
   if (lane == 0) out[blockIdx.x * 4 + warp] = t1 - t0;
   sink[blockIdx.x * 128 + threadIdx.x] = acc;
   tc_fence_before();
-  __syncthreads();
+  asm volatile("bar.sync 1, 128;");
   if (warp == 0) tmem_dealloc<512>(tb_s);
 }
 
-template <int VAR>
+template <int VAR, int BG = 0>
 void run(const char* name, int nsm) {
+  static float* gsrc = nullptr;
+  if (!gsrc) cudaMalloc(&gsrc, (size_t)32768 * 8192 * 4);
   unsigned long long* d;
   float* sink;
   cudaMalloc(&d, nsm * 4 * 8);
   cudaMalloc(&sink, nsm * 128 * 4);
-  cudaFuncSetAttribute(split_kernel<VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
+  cudaFuncSetAttribute(split_kernel<VAR, BG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140000);
   const int iters = 2000;
-  split_kernel<VAR><<<nsm, 128, 70000>>>(10, d, sink);
-  split_kernel<VAR><<<nsm, 128, 70000>>>(iters, d, sink);
+  split_kernel<VAR, BG><<<nsm, 160, 140000>>>(10, d, sink, gsrc);
+  split_kernel<VAR, BG><<<nsm, 160, 140000>>>(iters, d, sink, gsrc);
   cudaError_t e = cudaDeviceSynchronize();
   std::vector<unsigned long long> h(nsm * 4);
   cudaMemcpy(h.data(), d, h.size() * 8, cudaMemcpyDeviceToHost);
@@ -109,6 +136,8 @@ void run(const char* name, int nsm) {
 int main() {
   int nsm = 148;
   run<0>("full: LDS + split + 3x STTM.x32 + wait", nsm);
+  run<0, 1>("full + background bulk copies (TMA-like)", nsm);
+  run<1, 1>("no TMEM store + background bulk copies", nsm);
   run<1>("no TMEM store", nsm);
   run<2>("STTM without per-chunk wait", nsm);
   run<3>("no LDS (register data) + STTM + wait", nsm);
