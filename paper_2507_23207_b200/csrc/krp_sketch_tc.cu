@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  pdl_launch_dependents();  // the assembly kernel may be scheduled now (it waits for this grid to finish)
 
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * p.T / gridDim.x;
   const int64_t t1 = static_cast<int64_t>(blockIdx.x + 1) * p.T / gridDim.x;
@@ -508,6 +509,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // warps 8-11: P side (z1 -> A1 += z1·Ω_S), warps 12-15: Q side (z2 -> A2 += z2·Ω_S); A1/A2 live
     // in TMEM (lane = ρ resp. γ).  T(s,r) = Σ_ρ z1·W_L = Σ_γ z2·W_R: its 8-column rounds alternate
     // between the two sides.
+    pdl_wait();  // B images and Ω_S rows come from the tables kernel launched just before
     const uint32_t ew = warp - kEpiWarp0;  // 0..7
     const uint32_t sub = warp & 3;         // TMEM lane quarter
     const bool pside = ew < 4;
@@ -546,9 +548,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (pair != prev_pair) {
         if (prev_pair >= 0)
         {  // flush the finished segment's accumulators into its partial slot
-          const int64_t slot = prev_pair * p.maxseg + (blockIdx.x - cta_of_tile(prev_pair * p.S, p.T, gridDim.x));
+          const int kslot = static_cast<int>(blockIdx.x - cta_of_tile(prev_pair * p.S, p.T, gridDim.x));
+          const int64_t slot = prev_pair * p.maxseg + kslot;
           if (threadIdx.x == kEpiWarp0 * 32) p.slot_pair[slot] = static_cast<int>(prev_pair);
           float* dst = (pside ? p.partA1 : p.partA2) + (slot * kTile + l) * R;
+          // the CTA holding the pair's last tile zero-fills the pair's unused trailing slots, so the
+          // assembly can sum all maxseg slots of every pair (adding +0 is exact)
+          if (active && (prev_pair + 1) * p.S <= t1)
+            for (int k2 = kslot + 1; k2 < p.maxseg; ++k2)
+              for (int j = 0; j < R; ++j) dst[static_cast<int64_t>(k2 - kslot) * kTile * R + j] = 0.f;
           if constexpr (RA > 0) {
 #pragma unroll
             for (int j = 0; j < RA; ++j) {
@@ -663,9 +671,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (prev_pair >= 0)
         {  // flush the finished segment's accumulators into its partial slot
-          const int64_t slot = prev_pair * p.maxseg + (blockIdx.x - cta_of_tile(prev_pair * p.S, p.T, gridDim.x));
+          const int kslot = static_cast<int>(blockIdx.x - cta_of_tile(prev_pair * p.S, p.T, gridDim.x));
+          const int64_t slot = prev_pair * p.maxseg + kslot;
           if (threadIdx.x == kEpiWarp0 * 32) p.slot_pair[slot] = static_cast<int>(prev_pair);
           float* dst = (pside ? p.partA1 : p.partA2) + (slot * kTile + l) * R;
+          // the CTA holding the pair's last tile zero-fills the pair's unused trailing slots, so the
+          // assembly can sum all maxseg slots of every pair (adding +0 is exact)
+          if (active && (prev_pair + 1) * p.S <= t1)
+            for (int k2 = kslot + 1; k2 < p.maxseg; ++k2)
+              for (int j = 0; j < R; ++j) dst[static_cast<int64_t>(k2 - kslot) * kTile * R + j] = 0.f;
           if constexpr (RA > 0) {
 #pragma unroll
             for (int j = 0; j < RA; ++j) {
@@ -705,25 +719,27 @@ struct TabParams {
 // lo = W - hi, other rows are zero.  W_L(ρ,r) = Π_{k<m} Ω_k(i_k(ρ),r) for the row blocks (BQimg),
 // W_R(γ,r) = Π_{m<=k<m2} Ω_k(i_k(γ),r) for the col blocks (BPimg).  OmS(s,r) = Π_{k>=m2} Ω_k(i_k(s),r).
 __global__ void tc_tables_kernel(const __grid_constant__ TabParams p) {
-  int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t per_blk = static_cast<int64_t>(p.NP) * kTile;
-  const int64_t nq = p.RB * per_blk, np_ = p.CB * per_blk, ns = p.S * p.RS;
+  // 32-bit index math throughout: the plan guarantees every table and group size is below 2^31
+  uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t per_blk = static_cast<uint32_t>(p.NP) * kTile;
+  const uint32_t nq = static_cast<uint32_t>(p.RB) * per_blk, np_ = static_cast<uint32_t>(p.CB) * per_blk;
+  const uint32_t ns = static_cast<uint32_t>(p.S) * static_cast<uint32_t>(p.RS);
   if (idx < nq + np_) {
     const bool rows = idx < nq;
     if (!rows) idx -= nq;
-    const int64_t blk = idx / per_blk;
-    const int rem = static_cast<int>(idx - blk * per_blk);
+    const uint32_t blk = idx / per_blk;
+    const uint32_t rem = idx - blk * per_blk;
     // rem enumerates (n, l) with l fastest
-    const int n = rem / kTile, l = rem % kTile;
-    const int64_t lin = blk * kTile + l;
+    const int n = static_cast<int>(rem / kTile), l = static_cast<int>(rem % kTile);
+    const uint32_t lin = blk * kTile + l;
     float v = 0.f;
     const int r = n < p.R ? n : (n >= p.R8 && n < p.R8 + p.R ? n - p.R8 : -1);
-    if (r >= 0 && lin < (rows ? p.M : p.C)) {
+    if (r >= 0 && lin < static_cast<uint32_t>(rows ? p.M : p.C)) {
       float w = 1.f;
       for (int k = rows ? 0 : p.m; k < (rows ? p.m : p.m2); ++k) {
         if (!p.om[k]) continue;  // Ω_n of a single-mode sketch is not given: it never reaches Y_n
-        const int64_t ik = (lin / p.gs[k]) % p.n[k];
-        w *= __ldg(p.om[k] + ik * p.R + r);
+        const uint32_t ik = (lin / static_cast<uint32_t>(p.gs[k])) % static_cast<uint32_t>(p.n[k]);
+        w *= __ldg(p.om[k] + static_cast<size_t>(ik) * p.R + r);
       }
       const float whi = __uint_as_float(tf32_hi_bits(w));
       v = (n < p.R) ? whi : w - whi;
@@ -731,18 +747,18 @@ __global__ void tc_tables_kernel(const __grid_constant__ TabParams p) {
     const uint32_t k32 = static_cast<uint32_t>(l) & 31u;
     const size_t off = static_cast<size_t>(l >> 5) * (p.NP * 128) + static_cast<size_t>(n) * 128 +
                        (((k32 >> 2) ^ (static_cast<uint32_t>(n) & 7u)) << 4) + (k32 & 3u) * 4u;
-    float* img = (rows ? p.BQimg : p.BPimg) + blk * per_blk;
+    float* img = (rows ? p.BQimg : p.BPimg) + static_cast<size_t>(blk) * per_blk;
     *reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(img) + off) = v;
   } else if ((idx -= nq + np_) < ns) {
-    const int64_t sl = idx / p.RS;
-    const int r = static_cast<int>(idx - sl * p.RS);
+    const uint32_t sl = idx / static_cast<uint32_t>(p.RS);
+    const int r = static_cast<int>(idx - sl * static_cast<uint32_t>(p.RS));
     float w = 0.f;
     if (r < p.R) {
       w = 1.f;
       for (int k = p.m2; k < p.d; ++k) {
         if (!p.om[k]) continue;
-        const int64_t ik = (sl / p.gs[k]) % p.n[k];
-        w *= __ldg(p.om[k] + ik * p.R + r);
+        const uint32_t ik = (sl / static_cast<uint32_t>(p.gs[k])) % static_cast<uint32_t>(p.n[k]);
+        w *= __ldg(p.om[k] + static_cast<size_t>(ik) * p.R + r);
       }
     }
     p.OmS[idx] = w;
@@ -756,17 +772,20 @@ struct RedParams {
   int do_p, do_q, do_t;
   const float *partA1, *partA2, *Tpart;
   float *Pm, *Qc, *Ts;
+  float *outP, *outQ, *outT;  // non-null: the group is a single wanted mode, write its Y directly
 };
 
-// P(ρ,r) = Σ_{cb} Σ_{CTAs b of pair (rb,cb)} partA1[slot(b,pair)][ρ%128][r]
+// P(ρ,r) = Σ_{cb} Σ_{k < maxseg} partA1[(rb*CB + cb)*maxseg + k][ρ%128][r]   (unused slots are zero)
 // Qc(γ,r) likewise over rb;  Ts(s,r) = Σ_{pairs} Tpart[pair][s][r].
-// One block = 32 consecutive outputs (lanes, coalesced) x 8 warps; warp w sums its fixed share of the
-// terms in order, then warp 0 adds the 8 warp sums in order: a fixed reduction tree (deterministic)
-// whose depth is terms/8 instead of terms.  A block never straddles a 128-row block (32 | 128*R) nor
-// a region (regions are padded to whole blocks).
+// One block = 32 consecutive outputs (lanes, coalesced) x 8 warps; the flattened term list is split into
+// 8 contiguous shares, each summed in order with its loads issued 8 at a time, then warp 0 adds the 8
+// shares in order: a fixed reduction tree (deterministic).  A block never straddles a 128-row block
+// (32 | 128*R) nor a region (regions are padded to whole blocks).  A group with a single mode IS that
+// mode's sketch, so its region is written straight into Y (outP / outQ / outT non-null).
 constexpr int kRedWarps = 8;
 __global__ void __launch_bounds__(256) tc_assemble_kernel(const __grid_constant__ RedParams p) {
   __shared__ float red[kRedWarps][32];
+  pdl_wait();  // the partials are written by the sketch kernel
   const int w = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
   const int64_t nP = p.do_p ? p.M * p.R : 0, nQ = p.do_q ? p.C * p.R : 0, nT = p.do_t ? p.S * p.R : 0;
   const int64_t bP = (nP + 31) / 32, bQ = (nQ + 31) / 32;
@@ -785,29 +804,35 @@ __global__ void __launch_bounds__(256) tc_assemble_kernel(const __grid_constant_
   if (region < 2) {
     const bool rows = region == 0;
     const int64_t n = rows ? nP : nQ;
-    const int64_t lin = (idx < n ? idx : n - 1) / p.R;
-    const int r = static_cast<int>((idx < n ? idx : n - 1) - lin * p.R);
+    const uint32_t ic = static_cast<uint32_t>(idx < n ? idx : n - 1);
+    const uint32_t lin = ic / static_cast<uint32_t>(p.R);
+    const int r = static_cast<int>(ic - lin * static_cast<uint32_t>(p.R));
     const int blk = static_cast<int>(lin / kTile), l = static_cast<int>(lin % kTile);
-    const float* part = rows ? p.partA1 : p.partA2;
-    const int nother = rows ? p.CB : p.RB;
+    const float* part = (rows ? p.partA1 : p.partA2) + static_cast<int64_t>(l) * p.R + r;
     const int64_t kstride = static_cast<int64_t>(kTile) * p.R;
-    for (int o = 0; o < nother; ++o) {
-      const int64_t pair = rows ? (static_cast<int64_t>(blk) * p.CB + o) : (static_cast<int64_t>(o) * p.CB + blk);
-      const int nk = cta_of_tile((pair + 1) * p.S - 1, p.T, p.grid) - cta_of_tile(pair * p.S, p.T, p.grid) + 1;
-      const int k0 = w * nk / kRedWarps, k1 = (w + 1) * nk / kRedWarps;
-      const float* src = part + ((pair * p.maxseg) * kTile + l) * p.R + r;
-      for (int k = k0; k < k1; k += 8) {
-        float v[8];
+    const int nother = rows ? p.CB : p.RB;
+    const int64_t F = static_cast<int64_t>(nother) * p.maxseg;  // flattened (other block, slot) terms
+    const int64_t f0 = w * F / kRedWarps, f1 = (w + 1) * F / kRedWarps;
+    for (int64_t f = f0; f < f1; f += 8) {
+      float v[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = (k + i < k1) ? __ldg(src + (k + i) * kstride) : 0.f;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc += v[i];
+      for (int i = 0; i < 8; ++i) {
+        v[i] = 0.f;
+        const int64_t ff = f + i;
+        if (ff < f1) {
+          const uint32_t f32 = static_cast<uint32_t>(ff), o = f32 / static_cast<uint32_t>(p.maxseg);
+          const uint32_t k = f32 - o * static_cast<uint32_t>(p.maxseg);
+          const int64_t pair = rows ? (static_cast<int64_t>(blk) * p.CB + o) : (static_cast<int64_t>(o) * p.CB + blk);
+          v[i] = __ldg(part + (pair * p.maxseg + k) * kstride);
+        }
       }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc += v[i];
     }
   } else {
-    const int64_t idc = idx < nT ? idx : nT - 1;
-    const int64_t s = idc / p.R;
-    const int r = static_cast<int>(idc - s * p.R);
+    const uint32_t idc = static_cast<uint32_t>(idx < nT ? idx : nT - 1);
+    const uint32_t s = idc / static_cast<uint32_t>(p.R);
+    const int r = static_cast<int>(idc - s * static_cast<uint32_t>(p.R));
     const int64_t npairs = static_cast<int64_t>(p.RB) * p.CB;
     const int64_t p0 = w * npairs / kRedWarps, p1 = (w + 1) * npairs / kRedWarps;
     const int64_t pstride = p.S * p.R;
@@ -827,7 +852,8 @@ __global__ void __launch_bounds__(256) tc_assemble_kernel(const __grid_constant_
 #pragma unroll
     for (int i = 1; i < kRedWarps; ++i) tot += red[i][lane];
     const int64_t n = region == 0 ? nP : (region == 1 ? nQ : nT);
-    if (idx < n) (region == 0 ? p.Pm : (region == 1 ? p.Qc : p.Ts))[idx] = tot;
+    float* out = region == 0 ? (p.outP ? p.outP : p.Pm) : (region == 1 ? (p.outQ ? p.outQ : p.Qc) : (p.outT ? p.outT : p.Ts));
+    if (idx < n) out[idx] = tot;
   }
 }
 
@@ -850,6 +876,7 @@ struct TtvParams {
 // Same block shape as the assembly: 32 outputs x 8 warps splitting the o range, fixed-order combine.
 __global__ void __launch_bounds__(256) tc_ttv_kernel(const __grid_constant__ TtvParams p) {
   __shared__ double red[kRedWarps][32];
+  pdl_wait();  // the group objects are written by the assembly kernel
   const int w = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
   int64_t blk_id = blockIdx.x;
   int k = 0;
@@ -863,9 +890,9 @@ __global__ void __launch_bounds__(256) tc_ttv_kernel(const __grid_constant__ Ttv
   }
   if (k >= p.d) return;
   const int64_t idx = blk_id * 32 + lane;
-  const int64_t idc = idx < cnt ? idx : cnt - 1;
-  const int64_t i = idc / p.R;
-  const int r = static_cast<int>(idc - i * p.R);
+  const uint32_t idc = static_cast<uint32_t>(idx < cnt ? idx : cnt - 1);
+  const uint32_t i = idc / static_cast<uint32_t>(p.R);
+  const int r = static_cast<int>(idc - i * static_cast<uint32_t>(p.R));
   int g0, g1;
   const float* src;
   int64_t gsize;
@@ -887,16 +914,16 @@ __global__ void __launch_bounds__(256) tc_ttv_kernel(const __grid_constant__ Ttv
       wv[u] = 0.f;
       const int64_t o = ob + u;
       if (o < o1) {
-        int64_t rem = o, lin = i * p.gs[k];
+        uint32_t rem = static_cast<uint32_t>(o), lin = i * static_cast<uint32_t>(p.gs[k]);
         float wt = 1.f;
         for (int j = g0; j < g1; ++j) {
           if (j == k) continue;
-          const int64_t ij = rem % p.n[j];
-          rem /= p.n[j];
-          lin += ij * p.gs[j];
-          wt *= __ldg(p.om[j] + ij * p.R + r);
+          const uint32_t nj = static_cast<uint32_t>(p.n[j]), q = rem / nj, ij = rem - q * nj;
+          rem = q;
+          lin += ij * static_cast<uint32_t>(p.gs[j]);
+          wt *= __ldg(p.om[j] + static_cast<size_t>(ij) * p.R + r);
         }
-        xv[u] = __ldg(src + lin * p.R + r);
+        xv[u] = __ldg(src + static_cast<size_t>(lin) * p.R + r);
         wv[u] = wt;
       }
     }
@@ -909,7 +936,7 @@ __global__ void __launch_bounds__(256) tc_ttv_kernel(const __grid_constant__ Ttv
     double tot = red[0][lane];
 #pragma unroll
     for (int u = 1; u < kRedWarps; ++u) tot += red[u][lane];
-    if (idx < cnt) p.y[k][i * p.R + r] = static_cast<float>(tot);
+    if (idx < cnt) p.y[k][static_cast<size_t>(i) * p.R + r] = static_cast<float>(tot);
   }
 }
 
@@ -962,7 +989,9 @@ bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, TcPlan& pl
   for (int k = m; k < m2; ++k) C *= g.n[k];
   for (int k = m2; k < g.d; ++k) S *= g.n[k];
   if (M < kTile || C < kTile || (M % 4) != 0) return false;
-  if (M > (int64_t(1) << 31) || C > (int64_t(1) << 31) || S > (int64_t(1) << 31)) return false;
+  // the table / assembly kernels use 32-bit index math
+  if (M * kMaxTcR >= (int64_t(1) << 31) || C * kMaxTcR >= (int64_t(1) << 31) || S * kMaxTcR >= (int64_t(1) << 31))
+    return false;
   bool wr = false, wc = false, ws = false;
   for (int k = 0; k < g.d; ++k) {
     if (!want[k]) continue;
@@ -1272,7 +1301,7 @@ int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const b
   KRP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(pl.smem_bytes)));
   prof_begin(s);
-  kern<<<pl.grid, kThreads, pl.smem_bytes, s>>>(tmap, p);
+  KRP_CHECK_CUDA(launch_pdl(kern, dim3(pl.grid), dim3(kThreads), pl.smem_bytes, s, tmap, p));
   KRP_CHECK_LAUNCH();
   prof_end(s, 4.0 * static_cast<double>(g.N), 2.0 * static_cast<double>(g.N) * R * (pl.do_p + pl.do_q));
   if (p.trace) {  // development: dump CTA 0's role timeline (KRP_TC_TRACE=<file>)
@@ -1305,8 +1334,11 @@ int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const b
     rp.Pm = Pm;
     rp.Qc = Qc;
     rp.Ts = Ts;
+    rp.outP = (pl.m == 1 && want[0]) ? Y[0] : nullptr;
+    rp.outQ = (pl.m2 - pl.m == 1 && want[pl.m]) ? Y[pl.m] : nullptr;
+    rp.outT = (g.d - pl.m2 == 1 && want[pl.m2]) ? Y[pl.m2] : nullptr;
     const int64_t nblk = assemble_blocks(pl.M, pl.C, pl.S, R, pl.do_p, pl.do_q, pl.do_t);
-    tc_assemble_kernel<<<static_cast<unsigned>(nblk), 256, 0, s>>>(rp);
+    KRP_CHECK_CUDA(launch_pdl(tc_assemble_kernel, dim3(static_cast<unsigned>(nblk)), dim3(256), 0, s, rp));
     KRP_CHECK_LAUNCH();
   }
   {
@@ -1323,15 +1355,19 @@ int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const b
       tv.n[k] = g.n[k];
       tv.gs[k] = gs[k];
       tv.om[k] = om.p[k];
-      tv.want[k] = want[k] ? 1 : 0;
-      tv.y[k] = want[k] ? Y[k] : nullptr;
-      if (want[k]) nout += (g.n[k] * R + 31) / 32;
+      // single-mode groups were written by the assembly
+      const bool single = (k < pl.m) ? (pl.m == 1) : (k < pl.m2 ? (pl.m2 - pl.m == 1) : (g.d - pl.m2 == 1));
+      tv.want[k] = (want[k] && !single) ? 1 : 0;
+      tv.y[k] = tv.want[k] ? Y[k] : nullptr;
+      if (tv.want[k]) nout += (g.n[k] * R + 31) / 32;
     }
     tv.Pm = Pm;
     tv.Qc = Qc;
     tv.Ts = Ts;
-    tc_ttv_kernel<<<static_cast<unsigned>(nout), 256, 0, s>>>(tv);
-    KRP_CHECK_LAUNCH();
+    if (nout > 0) {
+      KRP_CHECK_CUDA(launch_pdl(tc_ttv_kernel, dim3(static_cast<unsigned>(nout)), dim3(256), 0, s, tv));
+      KRP_CHECK_LAUNCH();
+    }
   }
   ar.off = mark;
   return KRP_OK;
