@@ -72,7 +72,8 @@ struct TcParams {
   const float* OmS;    // [S][RS]: Khatri-Rao rows of the slice modes
   long long* trace;    // development timeline (KRP_TC_TRACE): CTA 0 role timestamps, null in production
   uint32_t wait_ns;    // mbarrier try_wait suspend-time hint (ns); 0 = spin
-  int dbg;             // development bottleneck probes (KRP_TC_DEBUG): 0 normal, 1 TMA only,
+  int dbg;             // development probes (KRP_TC_DEBUG bits): 1 no TMA data movement, 2 no MMAs, 4 no
+                       // epilogue math; results are garbage when set.  Legacy description follows:
                        // 2 TMA + split, 3 TMA + split + MMA (no epilogue), 4 TMA self-consumed
 };
 
@@ -91,7 +92,8 @@ __host__ __device__ __forceinline__ int cta_of_tile(int64_t t, int64_t T, int gr
 // every wait of the sketch kernel: try_wait with the plan's suspend-time hint (0 = plain spin)
 #define KWAIT(bar, par)                                              \
   do {                                                               \
-    if (p.wait_ns) mbar_wait_hint((bar), (par), p.wait_ns);          \
+    if (p.wait_ns >= 100000) mbar_wait_hint((bar), (par), p.wait_ns); \
+    else if (p.wait_ns) mbar_wait_sleep((bar), (par), p.wait_ns);    \
     else mbar_wait_spin((bar), (par));                               \
   } while (0)
 
@@ -313,10 +315,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (pf_t < t1) pf_issue();
         KWAIT(&empty_x[st], ph ^ 1);
         KRP_TRACE(0, t - t0);
-        mbar_arrive_expect_tx(&full_x[st], kStageFloats * 4);
-        float* dst = xs + st * kStageFloats;
-        for (int j = 0; j < 4; ++j)
-          tma_load_3d(dst + j * 4096, &tmap, &full_x[st], rb * kTile + 32 * j, cb * kTile, static_cast<int32_t>(s), pol);
+        if (p.dbg & 1) {  // probe: no data movement (the stage holds whatever it held)
+          mbar_arrive(&full_x[st]);
+        } else {
+          mbar_arrive_expect_tx(&full_x[st], kStageFloats * 4);
+          float* dst = xs + st * kStageFloats;
+          for (int j = 0; j < 4; ++j)
+            tma_load_3d(dst + j * 4096, &tmap, &full_x[st], rb * kTile + 32 * j, cb * kTile, static_cast<int32_t>(s),
+                        pol);
+        }
         if (++st == p.NS) {
           st = 0;
           ph ^= 1;
@@ -366,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t boff = static_cast<uint64_t>(kk0 >> 2) * katom_d + (kk0 & 3) * 2;
         // Q's A_hi: the raw tile in stage xst, box kk0/4 (16 KB), K offset (kk0 & 3) * 32 B
         const uint64_t aq = adesc_t + static_cast<uint64_t>(kk0 >> 2) * 1024 + (kk0 & 3) * 2;
-        if (leader) {
+        if (leader && !(p.dbg & 2)) {  // probe bit 2: no MMAs (handshakes only)
           if (p.triple) {
 #pragma unroll
             for (int ks = 0; ks < CH / 8; ++ks) {
@@ -438,9 +445,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (sub == 0 && lane == 0) KRP_TRACE(1, t - t0);
       const uint32_t stage_off = static_cast<uint32_t>(xst) * (kStageFloats * 4u);
       for (int kc = 0; kc < nkc; ++kc) {
-        KWAIT(&chunk_ready[cst], cph ^ 1);
-        if (sub == 0 && lane == 0) KRP_TRACE(8, (t - t0) * 8 + kc);
-        tc_fence_after();
+        if (sub == 0 && lane == 0) KRP_TRACE(13, (t - t0) * 8 + kc);
+        if (!(p.dbg & 8)) {  // probe bit 8: no slot wait / fences (garbage results)
+          KWAIT(&chunk_ready[cst], cph ^ 1);
+          if (sub == 0 && lane == 0) KRP_TRACE(8, (t - t0) * 8 + kc);
+          tc_fence_after();
+        }
         const uint32_t ch = tbase + lane_off + p.tm_chunk + cst * 3 * CH;
         // all shared-memory loads of the chunk first (one load latency per chunk)
         uint32_t px[CH], qv[CH];
@@ -488,8 +498,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (sub == 0 && lane == 0) KRP_TRACE(15, (t - t0) * 8 + kc);
         tmem_st_wait();
         if (sub == 0 && lane == 0) KRP_TRACE(9, (t - t0) * 8 + kc);
-        tc_fence_before();
+        if (!(p.dbg & 8)) tc_fence_before();
         __syncwarp();
+        if (sub == 0 && lane == 0) KRP_TRACE(12, (t - t0) * 8 + kc);
         if (lane == 0) mbar_arrive(&chunk_full[cst]);
         if (++cst == p.NC) {
           cst = 0;
@@ -610,6 +621,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       KWAIT(&acc_full[ast], aph);
+      if (p.dbg & 4) {  // probe: no epilogue math
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[ast]);
+        if (++ast == p.NA) {
+          ast = 0;
+          aph ^= 1;
+        }
+        continue;
+      }
       if (ew == 0 && lane == 0) KRP_TRACE(5, t - t0);
       tc_fence_after();
       const uint32_t tD = tbase + lane_off + p.tm_acc + ast * 2 * p.DN + (pside ? 0 : p.DN);

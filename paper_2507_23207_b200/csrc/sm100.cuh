@@ -70,6 +70,11 @@ __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Polling wait with a nanosleep back-off between probes: a sleeping warp issues nothing, so waiting warps
+// do not compete with the working warps for issue slots or for the shared-memory pipe.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  while (!mbar_try_wait(bar, parity)) __nanosleep(ns);
+}
 // Wait with an explicit suspend-time hint in nanoseconds (register operand).
 __device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity, uint32_t ns) {
   asm volatile(

@@ -32,6 +32,23 @@ __global__ void __launch_bounds__(160, 1) split_kernel(int iters, unsigned long 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  __shared__ uint64_t hs_full[2], hs_ready[2];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&hs_full[i], 4);
+      mbar_init(&hs_ready[i], 1);
+    }
+    fence_barrier_init();
+  }
+  asm volatile("bar.sync 2, 160;");
+  if (warp == 4 && VAR == 4) {  // partner: waits full[c], arrives ready[c] (like the MMA warp's commit)
+    for (int c = 0; c < iters * 4; ++c) {
+      mbar_wait(&hs_full[c & 1], (c >> 1) & 1);
+      if (elect_one()) mbar_arrive(&hs_ready[c & 1]);
+      __syncwarp();
+    }
+    return;
+  }
   if (warp == 4) {  // background bulk copies into a second 64 KB region (TMA-like SMEM writes)
     if (BG && elect_one()) {
       float* land = xs + 16384;
@@ -66,6 +83,11 @@ __global__ void __launch_bounds__(160, 1) split_kernel(int iters, unsigned long 
   long long t0 = clock64();
   for (int it = 0; it < iters; ++it) {
     for (int kc = 0; kc < 4; ++kc) {
+      const int c = it * 4 + kc;
+      if (VAR == 4 && c >= 2) {
+        mbar_wait(&hs_ready[c & 1], ((c >> 1) - 1) & 1);
+        tc_fence_after();
+      }
       const uint32_t ch = ch0 + (kc & 1) * 96;
       uint32_t px[32];
       float qv[32];
@@ -91,11 +113,16 @@ __global__ void __launch_bounds__(160, 1) split_kernel(int iters, unsigned long 
         ql[j] = __float_as_uint(m.x);
         ql[j + 1] = __float_as_uint(m.y);
       }
-      if (VAR == 0 || VAR == 2 || VAR == 3) {
+      if (VAR == 0 || VAR == 2 || VAR == 3 || VAR == 4) {
         tmem_st32(ch, px);
         tmem_st32(ch + 32, lo);
         tmem_st32(ch + 64, ql);
         if (VAR != 2) tmem_st_wait();
+        if (VAR == 4) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&hs_full[c & 1]);
+        }
       } else {
 #pragma unroll
         for (int j = 0; j < 32; ++j) acc += __uint_as_float(px[j] ^ lo[j] ^ ql[j]);
@@ -136,6 +163,7 @@ void run(const char* name, int nsm) {
 int main() {
   int nsm = 148;
   run<0>("full: LDS + split + 3x STTM.x32 + wait", nsm);
+  run<4>("full + fences + mbarrier handshake (NC=2)", nsm);
   run<0, 1>("full + background bulk copies (TMA-like)", nsm);
   run<1, 1>("no TMEM store + background bulk copies", nsm);
   run<1>("no TMEM store", nsm);
