@@ -40,12 +40,14 @@ namespace krp {
 namespace {
 using namespace sm100;
 
-constexpr int kNumSplitWarps = 4;  // one per TMEM lane quarter
-constexpr int kEpiWarp0 = kNumSplitWarps;
-constexpr int kNumEpiWarps = 8;    // (P | Q side) x TMEM lane quarter
-constexpr int kTmaWarp = kEpiWarp0 + kNumEpiWarps;
-constexpr int kMmaWarp = kTmaWarp + 1;  // issues every MMA and Q-view copy (and owns the TMEM allocation)
-constexpr int kThreads = (kMmaWarp + 1) * 32;
+// Five warpgroups.  setmaxnreg moves registers from the producer group to the epilogue groups.
+constexpr int kNumSplitWarps = 8;  // WG0-1: two per TMEM lane quarter; warp w fills chunk slot w / 4
+constexpr int kEpiWarp0 = 8;       // WG2-3: (P | Q side) x TMEM lane quarter
+constexpr int kNumEpiWarps = 8;
+constexpr int kTmaWarp = 16;       // WG4: TMA producer, MMA issuer (owns the TMEM allocation), 2 idle warps
+constexpr int kMmaWarp = 17;
+constexpr int kThreads = 20 * 32;
+constexpr int kRegsSplit = 96, kRegsEpi = 128, kRegsProd = 32;  // the epilogue gains exactly what the producer group releases: 256*(128-96) = 128*(96-32)
 constexpr int kTile = 128;
 constexpr int kStageFloats = 4 * 128 * 32;  // one 128x128 fp32 tile = 4 TMA boxes of {32, 128}
 constexpr int kMaxTcR = 64;
@@ -265,10 +267,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < p.NS; ++i) {
       mbar_init(&full_x[i], 1);
-      mbar_init(&empty_x[i], kNumSplitWarps + 1);
+      mbar_init(&empty_x[i], kNumSplitWarps + 1);  // all split warps + the MMA warp's commit
     }
     for (int i = 0; i < p.NC; ++i) {
-      mbar_init(&chunk_full[i], kNumSplitWarps);
+      mbar_init(&chunk_full[i], 4);  // the four split warps of this slot
       mbar_init(&chunk_ready[i], 1);
     }
     for (int i = 0; i < p.NA; ++i) {
@@ -289,6 +291,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int nkc = kTile / CH;
   const int64_t nchunks = (t1 - t0) * nkc;
 
+  if (warp >= kTmaWarp) {
+  // producer warpgroup: one setmaxnreg for the whole group, then TMA / MMA / idle warps
+  if (!(p.dbg & 16)) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsProd));
   if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer
     if (elect_one()) {
@@ -421,11 +426,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (++s_cur == p.S) s_cur = 0;
     }
+  }
   } else if (warp < kNumSplitWarps) {
+    // (two split warps per lane quarter: warp w processes the chunks of slot w / 4, i.e. kc % 2 == w / 4)
     // ------------------------------------------------------------ split warps: tile -> TMEM hi / lo
     // P view (lane = ρ): shared-memory loads (the transpose), hi = raw value, lo = x - tf32(x).
     // Q view (lane = γ): 16-byte loads of the rows; only lo goes to TMEM (Q's hi is read from SMEM).
     const uint32_t sub = warp & 3;
+    const int par = static_cast<int>(warp >> 2);  // chunk slot of this warp (NC == 2, nkc even)
     const uint32_t lane_off = (32u * sub) << 16;
     int xst = 0;
     uint32_t xph = 0;
@@ -438,29 +446,47 @@ __global__ void __launch_bounds__(kThreads, 1)
       psw[j] = smem_u32(xs) + sub * 16384u + ((((lane >> 2) ^ static_cast<uint32_t>(j)) << 4) | ((lane & 3u) << 2));
     const uint32_t gq = 32 * sub + lane;
     const uint32_t qrow = smem_u32(xs) + gq * 128u, qx = gq & 7u;
+    // chunk g of the CTA (all tiles) sits in slot g % NC; this warp takes the chunks with g % 2 == par
+    // (nkc is even, so that is kc % 2 == par in every tile); (cst, cph) track slot and phase of chunk g
     int cst = 0;
     uint32_t cph = 0;
+    auto advance = [&]() {
+      if (++cst == p.NC) {
+        cst = 0;
+        cph ^= 1;
+      }
+    };
+    if (par) advance();
     for (int64_t t = t0; t < t1; ++t) {
       KWAIT(&full_x[xst], xph);
       if (sub == 0 && lane == 0) KRP_TRACE(1, t - t0);
       const uint32_t stage_off = static_cast<uint32_t>(xst) * (kStageFloats * 4u);
-      for (int kc = 0; kc < nkc; ++kc) {
+      for (int kc = par; kc < nkc; kc += 2) {
         if (sub == 0 && lane == 0) KRP_TRACE(13, (t - t0) * 8 + kc);
-        if (!(p.dbg & 8)) {  // probe bit 8: no slot wait / fences (garbage results)
-          KWAIT(&chunk_ready[cst], cph ^ 1);
-          if (sub == 0 && lane == 0) KRP_TRACE(8, (t - t0) * 8 + kc);
-          tc_fence_after();
-        }
+        KWAIT(&chunk_ready[cst], cph ^ 1);
+        if (sub == 0 && lane == 0) KRP_TRACE(8, (t - t0) * 8 + kc);
+        tc_fence_after();
         const uint32_t ch = tbase + lane_off + p.tm_chunk + cst * 3 * CH;
-        // all shared-memory loads of the chunk first (one load latency per chunk)
-        uint32_t px[CH], qv[CH];
+        // P view: CH scalar loads (lane = ρ), hi stored as loaded, lo formed in place and stored
         if (dop) {
+          uint32_t px[CH];
           const uint32_t goff = stage_off + static_cast<uint32_t>(kc * CH) * 128u;
 #pragma unroll
           for (int j = 0; j < CH; ++j) px[j] = __float_as_uint(lds_f32(psw[j & 7] + goff + static_cast<uint32_t>(j) * 128u));
+          if (sub == 0 && lane == 0) KRP_TRACE(14, (t - t0) * 8 + kc);
+          tmem_st<CH>(ch + 0 * CH, px);  // hi: the raw value (the tensor core truncates to tf32)
+#pragma unroll
+          for (int j = 0; j < CH; j += 2) {
+            const float2 x = make_float2(__uint_as_float(px[j]), __uint_as_float(px[j + 1]));
+            const float2 l = f2_sub(x, make_float2(__uint_as_float(tf32_hi_bits(x.x)), __uint_as_float(tf32_hi_bits(x.y))));
+            px[j] = __float_as_uint(l.x);
+            px[j + 1] = __float_as_uint(l.y);
+          }
+          tmem_st<CH>(ch + 1 * CH, px);
         }
+        // Q view: lane = γ, columns ρ = kc*CH + j: CH consecutive ρ of row γ (16-byte chunks, swizzled)
         if (doq) {
-          // lane = γ, columns ρ = kc*CH + j: CH consecutive ρ of row γ (16-byte chunks, swizzled)
+          uint32_t qv[CH];
           const int rho0 = kc * CH;
           const uint32_t rowa = qrow + stage_off + static_cast<uint32_t>(rho0 >> 5) * 16384u;
 #pragma unroll
@@ -471,21 +497,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             qv[4 * qq] = __float_as_uint(a0), qv[4 * qq + 1] = __float_as_uint(a1);
             qv[4 * qq + 2] = __float_as_uint(a2), qv[4 * qq + 3] = __float_as_uint(a3);
           }
-        }
-        if (sub == 0 && lane == 0) KRP_TRACE(14, (t - t0) * 8 + kc);
-        if (dop) {
-          tmem_st<CH>(ch + 0 * CH, px);  // hi: the raw value (the tensor core truncates to tf32)
-          uint32_t lo[CH];
-#pragma unroll
-          for (int j = 0; j < CH; j += 2) {
-            const float2 x = make_float2(__uint_as_float(px[j]), __uint_as_float(px[j + 1]));
-            const float2 l = f2_sub(x, make_float2(__uint_as_float(tf32_hi_bits(x.x)), __uint_as_float(tf32_hi_bits(x.y))));
-            lo[j] = __float_as_uint(l.x);
-            lo[j + 1] = __float_as_uint(l.y);
-          }
-          tmem_st<CH>(ch + 1 * CH, lo);
-        }
-        if (doq) {
 #pragma unroll
           for (int j = 0; j < CH; j += 2) {
             const float2 x = make_float2(__uint_as_float(qv[j]), __uint_as_float(qv[j + 1]));
@@ -498,14 +509,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (sub == 0 && lane == 0) KRP_TRACE(15, (t - t0) * 8 + kc);
         tmem_st_wait();
         if (sub == 0 && lane == 0) KRP_TRACE(9, (t - t0) * 8 + kc);
-        if (!(p.dbg & 8)) tc_fence_before();
+        tc_fence_before();
         __syncwarp();
         if (sub == 0 && lane == 0) KRP_TRACE(12, (t - t0) * 8 + kc);
         if (lane == 0) mbar_arrive(&chunk_full[cst]);
-        if (++cst == p.NC) {
-          cst = 0;
-          cph ^= 1;
-        }
+        advance();  // skip the other parity's chunk
+        advance();
       }
       __syncwarp();
       if (sub == 0 && lane == 0) KRP_TRACE(2, t - t0);
@@ -520,6 +529,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // warps 8-11: P side (z1 -> A1 += z1·Ω_S), warps 12-15: Q side (z2 -> A2 += z2·Ω_S); A1/A2 live
     // in TMEM (lane = ρ resp. γ).  T(s,r) = Σ_ρ z1·W_L = Σ_γ z2·W_R: its 8-column rounds alternate
     // between the two sides.
+    if (!(p.dbg & 16)) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsEpi));  // both epilogue WGs
     pdl_wait();  // B images and Ω_S rows come from the tables kernel launched just before
     const uint32_t ew = warp - kEpiWarp0;  // 0..7
     const uint32_t sub = warp & 3;         // TMEM lane quarter
@@ -646,7 +656,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             epi_drain8(rnd, z8, tD, R, R8, p.triple);
 #pragma unroll
             for (int j = 0; j < 8; ++j) acc8[j] = Areg[8 * rnd + j];
-            epi_math8(rnd, z8, acc8, oms_g, p.do_t && ((rnd & 1) == (pside ? 0 : 1)), &wreg[8 * (rnd >> 1)], rbuf_s,
+            if (!(p.dbg & 64))  // probe bit 64: drain only
+            epi_math8(rnd, z8, acc8, oms_g, p.do_t && !(p.dbg & 32) && ((rnd & 1) == (pside ? 0 : 1)), &wreg[8 * (rnd >> 1)], rbuf_s,
                       R8, sub, lane);
 #pragma unroll
             for (int j = 0; j < 8; ++j) Areg[8 * rnd + j] = acc8[j];
@@ -677,7 +688,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ast = 0;
         aph ^= 1;
       }
-      if (p.do_t) {
+      if (p.do_t && !(p.dbg & 32)) {  // (probe bit 32: no T reduction)
         // fixed-order sum of the four lane quarters for every r (the two sides wrote disjoint rounds)
         named_bar_sync(2, kNumEpiWarps * 32);
         const int e = static_cast<int>(ew * 32 + lane);
@@ -1041,12 +1052,12 @@ bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, TcPlan& pl
   {
     struct Opt {
       int triple, na, ch, ncmin, areg;
-    } opts[8] = {{0, 2, 32, 2, 1}, {0, 2, 16, 4, 1}, {1, 2, 32, 2, 1}, {0, 2, 32, 2, 0},
+    } opts[9] = {{0, 2, 32, 2, 1}, {1, 2, 32, 3, 1}, {0, 2, 16, 4, 1}, {1, 2, 32, 2, 1}, {0, 2, 32, 2, 0},
                  {0, 2, 16, 3, 0}, {1, 2, 32, 2, 0}, {1, 2, 16, 2, 0}, {1, 1, 16, 2, 0}};
     pl.NC = 0;
     const char* force = getenv("KRP_TC_OPT");  // development: force one option (if it fits)
     const int fo = force ? atoi(force) : -1;
-    for (int oi = 0; oi < 8; ++oi) {
+    for (int oi = 0; oi < 9; ++oi) {
       const Opt& o = opts[oi];
       if (fo >= 0 && oi != fo) continue;
       if (o.areg && pl.R8 > 48) continue;  // register accumulators up to R = 48
