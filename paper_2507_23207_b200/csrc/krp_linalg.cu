@@ -348,19 +348,36 @@ __global__ void __launch_bounds__(256) jacobi_top_kernel(const double* __restric
   }
   __syncthreads();
   for (int sweep = 0; sweep < 40; ++sweep) {
-    if (tid == 0) {
+    {  // off-diagonal and total squared norms: per-thread partial sums, then a fixed-order warp tree
+      __shared__ double part_off[8], part_tot[8];
       double off = 0.0, tot = 0.0;
-      for (int i = 0; i < J; ++i)
-        for (int j = 0; j < J; ++j) {
-          const double v = A[i][j] * A[i][j];
-          tot += v;
-          if (i != j) off += v;
-        }
-      offn = off;
-      totn = tot;
+      for (int e = tid; e < 64 * 64; e += blockDim.x) {
+        const int i = e >> 6, j = e & 63;
+        if (i >= J || j >= J) continue;
+        const double v = A[i][j] * A[i][j];
+        tot += v;
+        if (i != j) off += v;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        off += __shfl_xor_sync(0xffffffffu, off, o);
+        tot += __shfl_xor_sync(0xffffffffu, tot, o);
+      }
+      if ((tid & 31) == 0) {
+        part_off[tid >> 5] = off;
+        part_tot[tid >> 5] = tot;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double so = 0.0, st = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) so += part_off[w], st += part_tot[w];
+        offn = so;
+        totn = st;
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    if (!(offn > 1e-30 * totn) || m < 2) break;
+    // converged when the off-diagonal mass is ~(1e-13)^2 of the total: eigenvectors are then accurate
+    // far below the fp32 output precision
+    if (!(offn > 1e-26 * totn) || m < 2) break;
     for (int round = 0; round < m - 1; ++round) {
       if (tid < m / 2) {
         int a, b;
@@ -385,11 +402,11 @@ __global__ void __launch_bounds__(256) jacobi_top_kernel(const double* __restric
         sn[tid] = s;
       }
       __syncthreads();
-      // rows: A <- J^T A
-      for (int e = tid; e < (m / 2) * J; e += blockDim.x) {
-        const int k = e / J, col = e % J;
+      // rows: A <- J^T A.  (pair k, column) slots as (e >> 6, e & 63): no integer division (J <= 64)
+      for (int e = tid; e < (m / 2) * 64; e += blockDim.x) {
+        const int k = e >> 6, col = e & 63;
         const int p = pp[k], q = qq[k];
-        if (q >= J) continue;
+        if (q >= J || col >= J) continue;
         const double c = cs[k], s = sn[k];
         const double ap = A[p][col], aq = A[q][col];
         A[p][col] = c * ap - s * aq;
@@ -397,10 +414,10 @@ __global__ void __launch_bounds__(256) jacobi_top_kernel(const double* __restric
       }
       __syncthreads();
       // columns: A <- A J ; V <- V J
-      for (int e = tid; e < (m / 2) * J; e += blockDim.x) {
-        const int k = e / J, row = e % J;
+      for (int e = tid; e < (m / 2) * 64; e += blockDim.x) {
+        const int k = e >> 6, row = e & 63;
         const int p = pp[k], q = qq[k];
-        if (q >= J) continue;
+        if (q >= J || row >= J) continue;
         const double c = cs[k], s = sn[k];
         const double ap = A[row][p], aq = A[row][q];
         A[row][p] = c * ap - s * aq;
