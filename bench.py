@@ -373,7 +373,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded Tucker/smooth tensors of BASELINE.json's configs; no dataset)",
-            "config": dict(_workload(cfg, world), engine=args.engine),
+            "config": _workload(cfg, world), "engine": args.engine,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "rhosvd_s": rhosvd_s, "rhosvd_rel_err": rel_err,
             "pct_roofline": 100.0 * max(t_hbm, t_tc) / (t_ms / 1e3 / args.steps),
