@@ -1369,7 +1369,13 @@ int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const b
     rp.outP = (pl.m == 1 && want[0]) ? Y[0] : nullptr;
     rp.outQ = (pl.m2 - pl.m == 1 && want[pl.m]) ? Y[pl.m] : nullptr;
     rp.outT = (g.d - pl.m2 == 1 && want[pl.m2]) ? Y[pl.m2] : nullptr;
-    const int64_t nblk = assemble_blocks(pl.M, pl.C, pl.S, R, pl.do_p, pl.do_q, pl.do_t);
+    if (rp.do_t && pl.RB * pl.CB == 1 && !rp.outT) {
+      // one (row block, col block) pair: the per-tile T rows already are Ts (same [s][r] layout), so the
+      // multi-TTV reads them in place and the assembly skips the slice region
+      Ts = p.Tpart;
+      rp.do_t = 0;
+    }
+    const int64_t nblk = assemble_blocks(pl.M, pl.C, pl.S, R, rp.do_p, rp.do_q, rp.do_t);
     KRP_CHECK_CUDA(launch_pdl(tc_assemble_kernel, dim3(static_cast<unsigned>(nblk)), dim3(256), 0, s, rp));
     KRP_CHECK_LAUNCH();
   }

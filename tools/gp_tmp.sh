@@ -1,2 +1,6 @@
-mkdir -p gpurun_out/d1
-timeout 300 python -m pytest tests/test_gpu_dist1.py -x -q > gpurun_out/d1/pytest.log 2>&1; echo "rc=$?" >> gpurun_out/d1/pytest.log
+mkdir -p gpurun_out/ab15
+timeout 300 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/ab15/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/ab15/pytest_gpu.log
+for c in c3 c4; do
+ echo "head"; KRP_LIB=$PWD/abtest/libkrp_head.so timeout 60 python tools/tc_time.py $c 20
+ echo "new"; timeout 60 python tools/tc_time.py $c 20 check
+done > gpurun_out/ab15/time.log 2>&1
