@@ -573,11 +573,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int64_t slot = prev_pair * p.maxseg + kslot;
           if (threadIdx.x == kEpiWarp0 * 32) p.slot_pair[slot] = static_cast<int>(prev_pair);
           float* dst = (pside ? p.partA1 : p.partA2) + (slot * kTile + l) * R;
-          // the CTA holding the pair's last tile zero-fills the pair's unused trailing slots, so the
-          // assembly can sum all maxseg slots of every pair (adding +0 is exact)
-          if (active && (prev_pair + 1) * p.S <= t1)
-            for (int k2 = kslot + 1; k2 < p.maxseg; ++k2)
-              for (int j = 0; j < R; ++j) dst[static_cast<int64_t>(k2 - kslot) * kTile * R + j] = 0.f;
+
           if constexpr (RA > 0) {
 #pragma unroll
             for (int j = 0; j < RA; ++j) {
@@ -707,11 +703,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int64_t slot = prev_pair * p.maxseg + kslot;
           if (threadIdx.x == kEpiWarp0 * 32) p.slot_pair[slot] = static_cast<int>(prev_pair);
           float* dst = (pside ? p.partA1 : p.partA2) + (slot * kTile + l) * R;
-          // the CTA holding the pair's last tile zero-fills the pair's unused trailing slots, so the
-          // assembly can sum all maxseg slots of every pair (adding +0 is exact)
-          if (active && (prev_pair + 1) * p.S <= t1)
-            for (int k2 = kslot + 1; k2 < p.maxseg; ++k2)
-              for (int j = 0; j < R; ++j) dst[static_cast<int64_t>(k2 - kslot) * kTile * R + j] = 0.f;
+
           if constexpr (RA > 0) {
 #pragma unroll
             for (int j = 0; j < RA; ++j) {
@@ -744,6 +736,9 @@ struct TabParams {
   int64_t gs[kMaxD];
   const float* om[kMaxD];
   float *BPimg, *BQimg, *OmS;
+  int64_t T;
+  int grid, npairs;
+  int* pnk;  // [npairs]: CTAs (partial slots) that touch each (row block, col block) pair
 };
 
 // B-operand images in the exact shared-memory layout the UMMA descriptors expect (K-major,
@@ -794,6 +789,9 @@ __global__ void tc_tables_kernel(const __grid_constant__ TabParams p) {
       }
     }
     p.OmS[idx] = w;
+  } else if ((idx -= ns) < static_cast<uint32_t>(p.npairs)) {
+    const int64_t pr = idx;
+    p.pnk[idx] = cta_of_tile((pr + 1) * p.S - 1, p.T, p.grid) - cta_of_tile(pr * p.S, p.T, p.grid) + 1;
   }
 }
 
@@ -803,11 +801,12 @@ struct RedParams {
   int RB, CB, R, grid, maxseg;
   int do_p, do_q, do_t;
   const float *partA1, *partA2, *Tpart;
+  const int* pnk;  // slots used per pair (slots k >= pnk[pair] are not read)
   float *Pm, *Qc, *Ts;
   float *outP, *outQ, *outT;  // non-null: the group is a single wanted mode, write its Y directly
 };
 
-// P(ρ,r) = Σ_{cb} Σ_{k < maxseg} partA1[(rb*CB + cb)*maxseg + k][ρ%128][r]   (unused slots are zero)
+// P(ρ,r) = Σ_{cb} Σ_{k < pnk[pair]} partA1[(rb*CB + cb)*maxseg + k][ρ%128][r]
 // Qc(γ,r) likewise over rb;  Ts(s,r) = Σ_{pairs} Tpart[pair][s][r].
 // One block = 32 consecutive outputs (lanes, coalesced) x 8 warps; the flattened term list is split into
 // 8 contiguous shares, each summed in order with its loads issued 8 at a time, then warp 0 adds the 8
@@ -855,7 +854,7 @@ __global__ void __launch_bounds__(256) tc_assemble_kernel(const __grid_constant_
           const uint32_t f32 = static_cast<uint32_t>(ff), o = f32 / static_cast<uint32_t>(p.maxseg);
           const uint32_t k = f32 - o * static_cast<uint32_t>(p.maxseg);
           const int64_t pair = rows ? (static_cast<int64_t>(blk) * p.CB + o) : (static_cast<int64_t>(o) * p.CB + blk);
-          v[i] = __ldg(part + (pair * p.maxseg + k) * kstride);
+          if (static_cast<int>(k) < __ldg(p.pnk + pair)) v[i] = __ldg(part + (pair * p.maxseg + k) * kstride);
         }
       }
 #pragma unroll
@@ -1147,7 +1146,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 long long* g_trace_dev = nullptr;
 
 struct WsLayout {
-  size_t a1, a2, slots, tpart, pm, qc, ts, wl, wr, oms, total;
+  size_t a1, a2, slots, pnk, tpart, pm, qc, ts, wl, wr, oms, total;
 };
 WsLayout ws_layout(const TcPlan& pl) {
   WsLayout w{};
@@ -1161,6 +1160,7 @@ WsLayout ws_layout(const TcPlan& pl) {
   w.a1 = take(pl.do_p ? slotf : 0);
   w.a2 = take(pl.do_q ? slotf : 0);
   w.slots = take(static_cast<size_t>(pl.nslot) * sizeof(int));
+  w.pnk = take(static_cast<size_t>(pl.RB) * pl.CB * sizeof(int));
   w.tpart = take(pl.do_t ? static_cast<size_t>(pl.RB) * pl.CB * pl.S * pl.R * sizeof(float) : 0);
   w.pm = take(static_cast<size_t>(pl.M) * pl.R * sizeof(float));
   w.qc = take(static_cast<size_t>(pl.C) * pl.R * sizeof(float));
@@ -1309,7 +1309,11 @@ int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const b
     tp.BPimg = BPimg;
     tp.BQimg = BQimg;
     tp.OmS = OmS;
-    const int64_t nt = (static_cast<int64_t>(pl.RB) + pl.CB) * pl.NP * kTile + pl.S * pl.RS;
+    tp.T = pl.T;
+    tp.grid = pl.grid;
+    tp.npairs = pl.RB * pl.CB;
+    tp.pnk = reinterpret_cast<int*>(wsb + wl.pnk);
+    const int64_t nt = (static_cast<int64_t>(pl.RB) + pl.CB) * pl.NP * kTile + pl.S * pl.RS + tp.npairs;
     tc_tables_kernel<<<static_cast<unsigned>((nt + 255) / 256), 256, 0, s>>>(tp);
     KRP_CHECK_LAUNCH();
   }
@@ -1363,6 +1367,7 @@ int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const b
     rp.partA1 = p.partA1;
     rp.partA2 = p.partA2;
     rp.Tpart = p.Tpart;
+    rp.pnk = reinterpret_cast<const int*>(wsb + wl.pnk);
     rp.Pm = Pm;
     rp.Qc = Qc;
     rp.Ts = Ts;
