@@ -74,6 +74,8 @@ struct TcParams {
   const float* OmS;    // [S][RS]: Khatri-Rao rows of the slice modes
   long long* trace;    // development timeline (KRP_TC_TRACE): CTA 0 role timestamps, null in production
   uint32_t wait_ns;    // mbarrier try_wait suspend-time hint (ns); 0 = spin
+  int mma_spin;        // 1: the MMA warp polls its barriers without a suspend hint
+  int split_spin;      // 1: the split warps poll chunk_ready without a suspend hint
   int dbg;             // development probes (KRP_TC_DEBUG bits): 1 no TMA data movement, 2 no MMAs, 4 no
                        // epilogue math; results are garbage when set.  Legacy description follows:
                        // 2 TMA + split, 3 TMA + split + MMA (no epilogue), 4 TMA self-consumed
@@ -363,14 +365,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         bph ^= 1;
         first = false;
       }
-      KWAIT(&acc_empty[ast], aph ^ 1);
+      if (p.mma_spin) mbar_wait_spin(&acc_empty[ast], aph ^ 1); else KWAIT(&acc_empty[ast], aph ^ 1);
       if (leader) KRP_TRACE(3, t - t0);
       tc_fence_after();
       const uint32_t dP = tbase + p.tm_acc + ast * 2 * p.DN;
       const uint32_t dQ = dP + p.DN;
         const uint64_t adesc_t = adesc0 + ((static_cast<uint64_t>(xst) * (kStageFloats * 4)) >> 4);
       for (int kc = 0; kc < nkc; ++kc) {
-        KWAIT(&chunk_full[cst], cph);
+        if (p.mma_spin) mbar_wait_spin(&chunk_full[cst], cph); else KWAIT(&chunk_full[cst], cph);
         if (leader) KRP_TRACE(10, (t - t0) * 8 + kc);
         tc_fence_after();
         const uint32_t ach = tbase + p.tm_chunk + cst * 3 * CH;  // [P hi | P lo | Q lo]
@@ -463,7 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t stage_off = static_cast<uint32_t>(xst) * (kStageFloats * 4u);
       for (int kc = par; kc < nkc; kc += 2) {
         if (sub == 0 && lane == 0) KRP_TRACE(13, (t - t0) * 8 + kc);
-        KWAIT(&chunk_ready[cst], cph ^ 1);
+        if (p.split_spin) mbar_wait_spin(&chunk_ready[cst], cph ^ 1); else KWAIT(&chunk_ready[cst], cph ^ 1);
         if (sub == 0 && lane == 0) KRP_TRACE(8, (t - t0) * 8 + kc);
         tc_fence_after();
         const uint32_t ch = tbase + lane_off + p.tm_chunk + cst * 3 * CH;
@@ -1262,6 +1264,10 @@ int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const b
     p.dbg = e ? atoi(e) : 0;
     const char* w = getenv("KRP_TC_WAIT_NS");
     p.wait_ns = w ? static_cast<uint32_t>(atol(w)) : 10000000u;
+    const char* ms = getenv("KRP_TC_MMA_SPIN");
+    p.mma_spin = ms ? atoi(ms) : 1;  // measured: c4 -9 %, c2 -1 % (profiles/r01f_ab_mma_spin.log)
+    const char* ss = getenv("KRP_TC_SPLIT_SPIN");
+    p.split_spin = ss ? atoi(ss) : 1;
     p.trace = nullptr;
     if (getenv("KRP_TC_TRACE")) {
       static long long* tr = nullptr;
