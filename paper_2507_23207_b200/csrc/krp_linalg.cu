@@ -69,44 +69,40 @@ __global__ void sum_partials_f64_kernel(const double* __restrict__ partial, int 
 // G (R x R, fp64) = L L^T.  Writes Linv (R x R row-major, lower) so that Q = Y Linv^T.
 // allow_shift: on breakdown, retry with G + s I, s = 11 (rows R + R(R+1)) u ||Y||_F^2 (flag |= 1);
 // a breakdown that cannot be shifted sets flag |= 2.
-__global__ void __launch_bounds__(128) chol_inv_kernel(const double* __restrict__ G, int R, int64_t rows,
-                                                       double* __restrict__ Linv_out, int* flag, int allow_shift) {
+__global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict__ G, int R, int64_t rows,
+                                                        double* __restrict__ Linv_out, int* flag, int allow_shift) {
   extern __shared__ double dyn_smem[];
   double(*A)[kGramMaxR + 1] = reinterpret_cast<double(*)[kGramMaxR + 1]>(dyn_smem);
   double(*Li)[kGramMaxR + 1] = reinterpret_cast<double(*)[kGramMaxR + 1]>(dyn_smem + kGramMaxR * (kGramMaxR + 1));
   __shared__ int fail;
   __shared__ double shift;
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    double tr = 0.0;
-    for (int i = 0; i < R; ++i) tr += G[i * R + i];
-    shift = 0.0;
-    (void)tr;
-  }
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (tid == 0) shift = 0.0;
   for (int attempt = 0; attempt < 2; ++attempt) {
     __syncthreads();
-    for (int e = tid; e < R * R; e += blockDim.x) {
+    for (int e = tid; e < R * R; e += nt) {
       const int i = e / R, j = e % R;
       A[i][j] = G[e] + (i == j ? shift : 0.0);
     }
     if (tid == 0) fail = 0;
     __syncthreads();
+    // right-looking Cholesky on the lower triangle: column j is final once the updates of columns < j
+    // have been applied; each step is a pivot, a column scale and a rank-1 trailing update
     for (int j = 0; j < R; ++j) {
-      if (tid == 0) {
-        double dgl = A[j][j];
-        for (int k = 0; k < j; ++k) dgl -= A[j][k] * A[j][k];
-        if (!(dgl > 0.0) || !isfinite(dgl)) {
-          fail = 1;
-        } else {
-          A[j][j] = sqrt(dgl);
-        }
+      const double dgl = A[j][j];
+      if (!(dgl > 0.0) || !isfinite(dgl)) {  // every thread reads the same value: a uniform exit
+        if (tid == 0) fail = 1;
+        break;
       }
+      const double ljj = sqrt(dgl);
+      __syncthreads();  // all threads have read A[j][j]
+      for (int i = j + 1 + tid; i < R; i += nt) A[i][j] /= ljj;
+      if (tid == 0) A[j][j] = ljj;
       __syncthreads();
-      if (fail) break;
-      for (int i = j + 1 + tid; i < R; i += blockDim.x) {
-        double v = A[i][j];
-        for (int k = 0; k < j; ++k) v -= A[i][k] * A[j][k];
-        A[i][j] = v / A[j][j];
+      const int t = R - j - 1;  // trailing (i, k), j < k <= i < R, as a t x t square slot grid
+      for (int e = tid; e < t * t; e += nt) {
+        const int i = j + 1 + e / t, k = j + 1 + e % t;
+        if (k <= i) A[i][k] -= A[i][j] * A[k][j];
       }
       __syncthreads();
     }
@@ -125,20 +121,25 @@ __global__ void __launch_bounds__(128) chol_inv_kernel(const double* __restrict_
   }
   __syncthreads();
   if (fail) {
-    for (int e = tid; e < R * R; e += blockDim.x) Linv_out[e] = 0.0;
+    for (int e = tid; e < R * R; e += nt) Linv_out[e] = 0.0;
     return;
   }
-  // column c of L^{-1} by forward substitution (one thread per column)
-  for (int c = tid; c < R; c += blockDim.x) {
-    for (int i = 0; i < R; ++i) Li[i][c] = 0.0;
-    for (int i = c; i < R; ++i) {
-      double s = (i == c) ? 1.0 : 0.0;
-      for (int k = c; k < i; ++k) s -= A[i][k] * Li[k][c];
-      Li[i][c] = s / A[i][i];
-    }
-  }
+  // L^{-1} by row-oriented forward elimination applied to the identity, all columns at once:
+  // row i is final after dividing by L[i][i]; it is then eliminated from the rows below it
+  for (int e = tid; e < R * R; e += nt) Li[e / R][e % R] = (e / R == e % R) ? 1.0 : 0.0;
   __syncthreads();
-  for (int e = tid; e < R * R; e += blockDim.x) Linv_out[e] = Li[e / R][e % R];
+  for (int i = 0; i < R; ++i) {
+    const double d = A[i][i];
+    for (int c = tid; c <= i; c += nt) Li[i][c] /= d;
+    __syncthreads();
+    const int t = R - i - 1;  // rows i+1..R-1, columns 0..i
+    for (int e = tid; e < t * (i + 1); e += nt) {
+      const int r = i + 1 + e / (i + 1), c = e % (i + 1);
+      Li[r][c] -= A[r][i] * Li[i][c];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < R * R; e += nt) Linv_out[e] = Li[e / R][e % R];
 }
 
 // Q[i][a] = sum_{b <= a} Y[i][b] * Linv[a][b]
@@ -157,13 +158,14 @@ __global__ void apply_linv_kernel(const T* __restrict__ Y, int64_t rows, int R, 
 
 __global__ void jacobi_top_kernel(const double* __restrict__ Hm, int J, int r, float* __restrict__ U);
 constexpr size_t kSquareSmem = 2 * kGramMaxR * (kGramMaxR + 1) * sizeof(double);
+constexpr size_t kJacobiSmem = 3 * kGramMaxR * (kGramMaxR + 1) * sizeof(double);
 int set_square_smem_attrs() {
   static int done = 0;
   if (!done) {
     KRP_CHECK_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(kSquareSmem)));
     KRP_CHECK_CUDA(cudaFuncSetAttribute(jacobi_top_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(kSquareSmem)));
+                                        static_cast<int>(kJacobiSmem)));
     done = 1;
   }
   return KRP_OK;
@@ -175,7 +177,7 @@ struct GramPlan {
 };
 GramPlan plan_gram(int64_t rows) {
   GramPlan g;
-  int64_t P = (rows + 127) / 128;
+  int64_t P = (rows + 31) / 32;  // one 32-row tile per block while that fills up to 256 blocks
   if (P > 256) P = 256;
   if (P < 1) P = 1;
   g.rows_per_block = ((rows + P - 1) / P + 31) / 32 * 32;
@@ -197,6 +199,9 @@ int gram(const T* Y, int64_t rows, int R, double* G, double* partial, cudaStream
 
 // ------------------------------------------------------------------ TTM
 // Y[l + L*(j + J*h)] = sum_i A[j*sj + i*si] * X[l + L*(i + I*h)]  (j in [j0, j0+64))
+// Generic layout: 64 (l,h) columns x 64 j per block, i in steps of 16.  Each thread's global offsets are
+// fixed across the i loop, so the (l, h) decomposition is done once; the next i step is prefetched into
+// registers while the current one is multiplied.
 __global__ void __launch_bounds__(256) ttm_kernel(const float* __restrict__ X, int64_t L, int64_t I, int64_t H,
                                                   const float* __restrict__ A, int J, int64_t sj, int64_t si,
                                                   float* __restrict__ Y, int j0) {
@@ -205,36 +210,54 @@ __global__ void __launch_bounds__(256) ttm_kernel(const float* __restrict__ X, i
   const int64_t P = L * H;
   const int64_t p0 = static_cast<int64_t>(blockIdx.x) * 64;
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  int xi[4], xp[4], ai[4], aj[4];
+  int64_t xoff[4];
+  const float* aptr[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int e = threadIdx.x + 256 * k;
+    if (L == 1) {
+      xi[k] = e % 16;
+      xp[k] = e / 16;
+    } else {
+      xp[k] = e % 64;
+      xi[k] = e / 64;
+    }
+    const int64_t p = p0 + xp[k];
+    xoff[k] = -1;
+    if (p < P) {
+      const int64_t l = p % L, h = p / L;
+      xoff[k] = l + L * I * h;
+    }
+    ai[k] = e % 16;
+    aj[k] = e / 16;
+    const int j = j0 + aj[k];
+    aptr[k] = j < J ? A + j * sj : nullptr;
+  }
+  float xr[4], ar[4];
+  auto fetch = [&](int64_t i0) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t i = i0 + xi[k];
+      xr[k] = (xoff[k] >= 0 && i < I) ? __ldg(X + xoff[k] + L * i) : 0.f;
+      const int64_t ia = i0 + ai[k];
+      ar[k] = (aptr[k] && ia < I) ? __ldg(aptr[k] + ia * si) : 0.f;
+    }
+  };
   float acc[4][4];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
+  fetch(0);
   for (int64_t i0 = 0; i0 < I; i0 += 16) {
-    for (int e = threadIdx.x; e < 1024; e += 256) {
-      int ii, pp;
-      if (L == 1) {
-        ii = e % 16;
-        pp = e / 16;
-      } else {
-        pp = e % 64;
-        ii = e / 64;
-      }
-      const int64_t p = p0 + pp, i = i0 + ii;
-      float v = 0.f;
-      if (p < P && i < I) {
-        const int64_t l = p % L, h = p / L;
-        v = __ldg(X + l + L * (i + I * h));
-      }
-      Xs[ii][pp] = v;
-    }
-    for (int e = threadIdx.x; e < 1024; e += 256) {
-      const int ii = e % 16, jj = e / 16;
-      const int j = j0 + jj;
-      const int64_t i = i0 + ii;
-      As[ii][jj] = (j < J && i < I) ? __ldg(A + j * sj + i * si) : 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      Xs[xi[k]][xp[k]] = xr[k];
+      As[ai[k]][aj[k]] = ar[k];
     }
     __syncthreads();
+    if (i0 + 16 < I) fetch(i0 + 16);
 #pragma unroll
     for (int ii = 0; ii < 16; ++ii) {
       float xv[4], av[4];
@@ -260,6 +283,116 @@ __global__ void __launch_bounds__(256) ttm_kernel(const float* __restrict__ X, i
       if (j < J) Y[l + L * (j + static_cast<int64_t>(J) * h)] = acc[a][b];
     }
   }
+}
+
+// Mode-0 TTM (L == 1, I % 4 == 0, 16-byte aligned X, J <= 64): Y[j + J*h] = sum_i A[j*sj + i*si] X[i + I*h],
+// i.e. the GEMM Y = A X with X column-major (each column h is I contiguous floats).  Block = 256 columns
+// h x all J rows; i in steps of 32 loaded as float4 (8 lanes cover one 128-byte column segment) and
+// transposed into Xs[i][h] (row stride 257: conflict-free stores and loads); warp ty owns rows
+// j = ty*NB + b (b < NB), lane tx owns columns tx + 32k (k < 8).  The output tile is staged through
+// shared memory so that the contiguous range Y[J*h0, J*(h0+256)) is written coalesced.
+constexpr int kM0Cols = 256, kM0K = 32, kM0XS = kM0Cols + 1;
+template <int NB>
+__global__ void __launch_bounds__(256, 2) ttm_mode0_kernel(const float* __restrict__ X, int64_t I, int64_t H,
+                                                           const float* __restrict__ A, int J, int64_t sj,
+                                                           int64_t si, float* __restrict__ Y) {
+  extern __shared__ float m0s[];
+  float* Xs = m0s;                        // [kM0K][kM0XS]
+  float* As = m0s + kM0K * kM0XS;         // [kM0K][64]: row ii, slot ty*8 + b
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  const int64_t h0 = static_cast<int64_t>(blockIdx.x) * kM0Cols;
+  // X tile loads: float4 f = tid + 256 k -> i quarter q = f % 8, column hh = f / 8
+  const float4* xptr[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int f = tid + 256 * k;
+    const int64_t h = h0 + (f >> 3);
+    xptr[k] = h < H ? reinterpret_cast<const float4*>(X + h * I) + (f & 7) : nullptr;
+  }
+  float4 xr[8];
+  float ar[8];
+  auto fetch = [&](int64_t i0) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const bool in = xptr[k] && i0 + 4 * ((tid + 256 * k) & 7) < I;
+      xr[k] = in ? __ldg(xptr[k] + (i0 >> 2)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const int e = tid + 256 * k;  // A slot: (ty', b) = e % 64 -> j = ty' * NB + b, ii = e / 64
+      const int ii = e >> 6, slot = e & 63, tyy = slot >> 3, b = slot & 7;
+      const int j = tyy * NB + b;
+      const int64_t i = i0 + ii;
+      ar[k] = (b < NB && j < J && i < I) ? __ldg(A + j * sj + i * si) : 0.f;
+    }
+  };
+  float acc[8][NB];
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) acc[k][b] = 0.f;
+  fetch(0);
+  for (int64_t i0 = 0; i0 < I; i0 += kM0K) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int f = tid + 256 * k, q = f & 7, hh = f >> 3;
+      Xs[(4 * q + 0) * kM0XS + hh] = xr[k].x;
+      Xs[(4 * q + 1) * kM0XS + hh] = xr[k].y;
+      Xs[(4 * q + 2) * kM0XS + hh] = xr[k].z;
+      Xs[(4 * q + 3) * kM0XS + hh] = xr[k].w;
+      const int e = tid + 256 * k;
+      As[e] = ar[k];
+    }
+    __syncthreads();
+    if (i0 + kM0K < I) fetch(i0 + kM0K);
+#pragma unroll 4
+    for (int ii = 0; ii < kM0K; ++ii) {
+      const float4 a0 = *reinterpret_cast<const float4*>(As + ii * 64 + ty * 8);
+      const float4 a1 = *reinterpret_cast<const float4*>(As + ii * 64 + ty * 8 + 4);
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float xv = Xs[ii * kM0XS + tx + 32 * k];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) acc[k][b] = fmaf(xv, av[b], acc[k][b]);
+      }
+    }
+    __syncthreads();
+  }
+  // stage the 256 x J output tile (row stride J + 1) and write it out contiguously
+  float* Ys = m0s;
+  const int JS = J + 1;
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int j = ty * NB + b;
+      if (j < J) Ys[(tx + 32 * k) * JS + j] = acc[k][b];
+    }
+  __syncthreads();
+  const int64_t ncols = min(static_cast<int64_t>(kM0Cols), H - h0);
+  const int total = static_cast<int>(ncols) * J;
+  float* out = Y + h0 * J;
+  for (int e = tid; e < total; e += 256) out[e] = Ys[(e / J) * JS + e % J];
+}
+
+size_t ttm_mode0_smem(int J) {
+  const size_t tiles = (static_cast<size_t>(kM0K) * kM0XS + kM0K * 64) * sizeof(float);
+  const size_t out = static_cast<size_t>(kM0Cols) * (J + 1) * sizeof(float);
+  return tiles > out ? tiles : out;
+}
+
+template <int NB>
+int launch_ttm_mode0(const float* X, int64_t I, int64_t H, const float* A, int J, int64_t sj, int64_t si, float* Y,
+                     cudaStream_t s) {
+  const size_t smem = ttm_mode0_smem(J);
+  static size_t set_bytes = 0;
+  if (smem > set_bytes) {
+    KRP_CHECK_CUDA(cudaFuncSetAttribute(ttm_mode0_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(ttm_mode0_smem(64))));
+    set_bytes = ttm_mode0_smem(64);
+  }
+  const unsigned nb = static_cast<unsigned>((H + kM0Cols - 1) / kM0Cols);
+  ttm_mode0_kernel<NB><<<nb, 256, smem, s>>>(X, I, H, A, J, sj, si, Y);
+  KRP_CHECK_LAUNCH();
+  return KRP_OK;
 }
 
 // ------------------------------------------------------------------ mode-n Gram
@@ -320,7 +453,7 @@ struct MGPlan {
 MGPlan plan_mode_gram(const Dims& g, int n) {
   const int64_t nf = g.N / g.n[n];
   MGPlan p;
-  int64_t P = (nf + 1023) / 1024;
+  int64_t P = (nf + 31) / 32;  // one 32-fiber tile per block while that fills up to 592 blocks
   if (P > 592) P = 592;
   if (P < 1) P = 1;
   p.per_block = ((nf + P - 1) / P + 31) / 32 * 32;
@@ -330,26 +463,62 @@ MGPlan plan_mode_gram(const Dims& g, int n) {
 }
 
 // ------------------------------------------------------------------ symmetric eigensolver (Jacobi)
-__global__ void __launch_bounds__(256) jacobi_top_kernel(const double* __restrict__ Hm, int J, int r,
-                                                         float* __restrict__ U) {
+// Parallel cyclic Jacobi (round-robin pairing: m-1 rounds of m/2 disjoint rotations per sweep).  One
+// round's update is ONE phase: thread (ki, kj) owns the 2x2 block of rows {p_ki, q_ki} x columns
+// {p_kj, q_kj}; it reads the two rotations from shared memory, writes the block of J^T A J into the
+// other A buffer and rotates its 2x2 block of V in place.  The m/2 rotations of a round are computed once
+// (fp64 divide/sqrt throughput makes per-block recomputation slower), so a round is two phases.
+__device__ __forceinline__ void jacobi_pair(int round, int k, int m, int& p, int& q) {
+  int a, b;
+  if (k == 0) {
+    a = m - 1;
+    b = round;
+  } else {
+    a = (round + k) % (m - 1);
+    b = (round - k + (m - 1)) % (m - 1);
+  }
+  p = a < b ? a : b;
+  q = a < b ? b : a;
+}
+
+__device__ __forceinline__ void jacobi_rot(const double (*A)[kGramMaxR + 1], int p, int q, int J, double& c,
+                                           double& s) {
+  c = 1.0;
+  s = 0.0;
+  if (q < J && A[p][q] != 0.0) {
+    const double tau = (A[q][q] - A[p][p]) / (2.0 * A[p][q]);
+    const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+    c = rsqrt(1.0 + t * t);
+    s = t * c;
+  }
+}
+
+__global__ void __launch_bounds__(1024) jacobi_top_kernel(const double* __restrict__ Hm, int J, int r,
+                                                          float* __restrict__ U) {
   extern __shared__ double dyn_smem[];
-  double(*A)[kGramMaxR + 1] = reinterpret_cast<double(*)[kGramMaxR + 1]>(dyn_smem);
-  double(*V)[kGramMaxR + 1] = reinterpret_cast<double(*)[kGramMaxR + 1]>(dyn_smem + kGramMaxR * (kGramMaxR + 1));
-  __shared__ double cs[kGramMaxR / 2], sn[kGramMaxR / 2];
-  __shared__ int pp[kGramMaxR / 2], qq[kGramMaxR / 2];
+  typedef double Row[kGramMaxR + 1];
+  Row* Abuf[2] = {reinterpret_cast<Row*>(dyn_smem), reinterpret_cast<Row*>(dyn_smem + kGramMaxR * (kGramMaxR + 1))};
+  Row* V = reinterpret_cast<Row*>(dyn_smem + 2 * kGramMaxR * (kGramMaxR + 1));
   __shared__ double offn, totn;
   __shared__ int order[kGramMaxR];
+  __shared__ double part_off[32], part_tot[32];
+  __shared__ double cs[kGramMaxR / 2], sn[kGramMaxR / 2];
+  __shared__ int pp[kGramMaxR / 2], qq[kGramMaxR / 2];
   const int tid = threadIdx.x;
   const int m = J + (J & 1);  // even number of players; index J (if odd J) is a dummy
+  const int half = m / 2;
+  const bool owner = tid < half * half;
+  const int ki = owner ? tid / half : 0, kj = owner ? tid % half : 0;
   for (int e = tid; e < J * J; e += blockDim.x) {
     const int i = e / J, j = e % J;
-    A[i][j] = Hm[e];
+    Abuf[0][i][j] = Hm[e];
     V[i][j] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
+  int cur = 0;
   for (int sweep = 0; sweep < 40; ++sweep) {
     {  // off-diagonal and total squared norms: per-thread partial sums, then a fixed-order warp tree
-      __shared__ double part_off[8], part_tot[8];
+      const Row* A = Abuf[cur];
       double off = 0.0, tot = 0.0;
       for (int e = tid; e < 64 * 64; e += blockDim.x) {
         const int i = e >> 6, j = e & 63;
@@ -379,56 +548,48 @@ __global__ void __launch_bounds__(256) jacobi_top_kernel(const double* __restric
     // far below the fp32 output precision
     if (!(offn > 1e-26 * totn) || m < 2) break;
     for (int round = 0; round < m - 1; ++round) {
-      if (tid < m / 2) {
-        int a, b;
-        if (tid == 0) {
-          a = m - 1;
-          b = round;
-        } else {
-          a = (round + tid) % (m - 1);
-          b = (round - tid + (m - 1)) % (m - 1);
-        }
-        const int p = a < b ? a : b, q = a < b ? b : a;
+      if (tid < half) {  // the round's m/2 rotations, once each
+        int p, q;
+        jacobi_pair(round, tid, m, p, q);
+        jacobi_rot(Abuf[cur], p, q, J, cs[tid], sn[tid]);
         pp[tid] = p;
         qq[tid] = q;
-        double c = 1.0, s = 0.0;
-        if (q < J && A[p][q] != 0.0) {
-          const double tau = (A[q][q] - A[p][p]) / (2.0 * A[p][q]);
-          const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-          c = 1.0 / sqrt(1.0 + t * t);
-          s = t * c;
+      }
+      __syncthreads();
+      if (owner) {
+        const Row* A = Abuf[cur];
+        Row* An = Abuf[cur ^ 1];
+        const int pi = pp[ki], qi = qq[ki], pj = pp[kj], qj = qq[kj];
+        const double ci = cs[ki], si = sn[ki], cj = cs[kj], sj = sn[kj];
+        const bool qiv = qi < J, qjv = qj < J;  // pi, pj < J always (the dummy is the larger index)
+        const double a00 = A[pi][pj];
+        const double a01 = qjv ? A[pi][qj] : 0.0;
+        const double a10 = qiv ? A[qi][pj] : 0.0;
+        const double a11 = (qiv && qjv) ? A[qi][qj] : 0.0;
+        // rows: A <- J^T A, then columns: A <- A J (the order of the two-phase formulation)
+        const double b00 = ci * a00 - si * a10, b01 = ci * a01 - si * a11;
+        const double b10 = si * a00 + ci * a10, b11 = si * a01 + ci * a11;
+        An[pi][pj] = cj * b00 - sj * b01;
+        if (qjv) An[pi][qj] = sj * b00 + cj * b01;
+        if (qiv) An[qi][pj] = cj * b10 - sj * b11;
+        if (qiv && qjv) An[qi][qj] = sj * b10 + cj * b11;
+        // V <- V J: rows {pi, qi}, columns {pj, qj}
+        if (qjv) {
+          const double vp = V[pi][pj], vq = V[pi][qj];
+          V[pi][pj] = cj * vp - sj * vq;
+          V[pi][qj] = sj * vp + cj * vq;
+          if (qiv) {
+            const double wp = V[qi][pj], wq = V[qi][qj];
+            V[qi][pj] = cj * wp - sj * wq;
+            V[qi][qj] = sj * wp + cj * wq;
+          }
         }
-        cs[tid] = c;
-        sn[tid] = s;
       }
-      __syncthreads();
-      // rows: A <- J^T A.  (pair k, column) slots as (e >> 6, e & 63): no integer division (J <= 64)
-      for (int e = tid; e < (m / 2) * 64; e += blockDim.x) {
-        const int k = e >> 6, col = e & 63;
-        const int p = pp[k], q = qq[k];
-        if (q >= J || col >= J) continue;
-        const double c = cs[k], s = sn[k];
-        const double ap = A[p][col], aq = A[q][col];
-        A[p][col] = c * ap - s * aq;
-        A[q][col] = s * ap + c * aq;
-      }
-      __syncthreads();
-      // columns: A <- A J ; V <- V J
-      for (int e = tid; e < (m / 2) * 64; e += blockDim.x) {
-        const int k = e >> 6, row = e & 63;
-        const int p = pp[k], q = qq[k];
-        if (q >= J || row >= J) continue;
-        const double c = cs[k], s = sn[k];
-        const double ap = A[row][p], aq = A[row][q];
-        A[row][p] = c * ap - s * aq;
-        A[row][q] = s * ap + c * aq;
-        const double vp = V[row][p], vq = V[row][q];
-        V[row][p] = c * vp - s * vq;
-        V[row][q] = s * vp + c * vq;
-      }
+      cur ^= 1;
       __syncthreads();
     }
   }
+  const Row* A = Abuf[cur];
   if (tid == 0) {
     for (int i = 0; i < J; ++i) order[i] = i;
     for (int t = 0; t < r; ++t) {  // selection of the r largest eigenvalues, descending
@@ -530,19 +691,19 @@ int cholqr(const float* Y, int64_t rows, int R, float* Qf, double* Qd, int* flag
   const unsigned nb = static_cast<unsigned>((tot + 255) / 256);
   // pass 1 (shift allowed)
   KRP_TRY(gram<float>(Y, rows, R, G, part, s));
-  chol_inv_kernel<<<1, 128, kSquareSmem, s>>>(G, R, rows, Li, flag_dev, 1);
+  chol_inv_kernel<<<1, 1024, kSquareSmem, s>>>(G, R, rows, Li, flag_dev, 1);
   KRP_CHECK_LAUNCH();
   apply_linv_kernel<float><<<nb, 256, 0, s>>>(Y, rows, R, Li, Q1, nullptr);
   KRP_CHECK_LAUNCH();
   // pass 2
   KRP_TRY(gram<double>(Q1, rows, R, G, part, s));
-  chol_inv_kernel<<<1, 128, kSquareSmem, s>>>(G, R, rows, Li, flag_dev, 0);
+  chol_inv_kernel<<<1, 1024, kSquareSmem, s>>>(G, R, rows, Li, flag_dev, 0);
   KRP_CHECK_LAUNCH();
   apply_linv_kernel<double><<<nb, 256, 0, s>>>(Q1, rows, R, Li, Q2, nullptr);
   KRP_CHECK_LAUNCH();
   // pass 3 (restores orthogonality after a shifted first pass; a no-op refinement otherwise)
   KRP_TRY(gram<double>(Q2, rows, R, G, part, s));
-  chol_inv_kernel<<<1, 128, kSquareSmem, s>>>(G, R, rows, Li, flag_dev, 0);
+  chol_inv_kernel<<<1, 1024, kSquareSmem, s>>>(G, R, rows, Li, flag_dev, 0);
   KRP_CHECK_LAUNCH();
   apply_linv_kernel<double><<<nb, 256, 0, s>>>(Q2, rows, R, Li, Qd, Qf);
   KRP_CHECK_LAUNCH();
@@ -554,6 +715,19 @@ int ttm(const float* X, const Dims& g, int n, const float* A, int J, int64_t sj,
         cudaStream_t s) {
   const int64_t L = g.stride[n], I = g.n[n], H = g.N / (L * I);
   const int64_t P = L * H;
+  if (P == 0 || J == 0) return KRP_OK;
+  if (L == 1 && J <= 64 && I % 4 == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 && H >= 148 * kM0Cols / 4) {
+    switch ((J + 7) / 8) {
+      case 1: return launch_ttm_mode0<1>(X, I, H, A, J, sj, si, Y, s);
+      case 2: return launch_ttm_mode0<2>(X, I, H, A, J, sj, si, Y, s);
+      case 3: return launch_ttm_mode0<3>(X, I, H, A, J, sj, si, Y, s);
+      case 4: return launch_ttm_mode0<4>(X, I, H, A, J, sj, si, Y, s);
+      case 5: return launch_ttm_mode0<5>(X, I, H, A, J, sj, si, Y, s);
+      case 6: return launch_ttm_mode0<6>(X, I, H, A, J, sj, si, Y, s);
+      case 7: return launch_ttm_mode0<7>(X, I, H, A, J, sj, si, Y, s);
+      default: return launch_ttm_mode0<8>(X, I, H, A, J, sj, si, Y, s);
+    }
+  }
   const unsigned nb = static_cast<unsigned>((P + 63) / 64);
   for (int j0 = 0; j0 < J; j0 += 64) {
     ttm_kernel<<<nb, 256, 0, s>>>(X, L, I, H, A, J, sj, si, Y, j0);
@@ -596,7 +770,7 @@ int sym_eig_top(const double* H, int J, int r, float* U, cudaStream_t s) {
     return KRP_EINVAL;
   }
   KRP_TRY(set_square_smem_attrs());
-  jacobi_top_kernel<<<1, 256, kSquareSmem, s>>>(H, J, r, U);
+  jacobi_top_kernel<<<1, 1024, kJacobiSmem, s>>>(H, J, r, U);
   KRP_CHECK_LAUNCH();
   return KRP_OK;
 }

@@ -147,7 +147,11 @@ def _check_factors(Q, ranks):
 
 
 @pytest.mark.parametrize("name,small", [("c1", None), ("c2", (128, 128, 128)), ("c4", (32, 32, 24, 24, 24)),
-                                        ("c5", (256, 256, 64))])
+                                        ("c5", (256, 256, 64)),
+                                        # mode-0 TTM kernel with ragged i (100 % 32) and column (10500 % 256) tails
+                                        ("c2", (100, 150, 70)),
+                                        # I_1 % 4 != 0: the generic TTM path for the large first contraction
+                                        ("c2", (99, 120, 90))])
 def test_rhosvd_parity(krp, name, small):
     cfg = synth.config(name) if small is None else synth.config(name).scaled(small)
     x = synth.tensor(cfg, 0)
