@@ -256,21 +256,24 @@ def rhosvd(x: np.ndarray, omegas: Sequence[np.ndarray], ranks: Sequence[int], ch
     1. Y_n = MTTKRP with the shared {Omega_k}       for every n
     2. Q_n = thin QR of Y_n, diag(R) > 0                    (l_n = R columns)
     3. G = X ×_1 Q_1ᵀ ... ×_d Q_dᵀ
-    4. if r_n < l_n: U_n = leading r_n left singular vectors of G_(n) (Alg. 2 pattern
-       P:118-120 applied to the core, S:371 recompression); Q_n <- Q_n U_n;
-       G <- G ×_n U_nᵀ  (modes in ascending order, each on the current G)
+    4. if r_n < l_n: U_n = leading r_n left singular vectors of G_(n) of the untruncated core
+       (HOSVD of the core: S:371 "hosvd on the core", Alg. 2 pattern P:118-120); Q_n <- Q_n U_n;
+       then G <- G ×_1 U_1ᵀ ... ×_d U_dᵀ
     5. relative error ||X - [G; Q]|| / ||X||
     Returns (qs, core, err, ys)."""
     d = x.ndim
     ys = sketch_all_modes(x, omegas, chunk)
     qs = [thin_qr(y)[0] for y in ys]
     g = _core_slabwise(x, qs, chunk)
+    us = [None] * d
     for n in range(d):
         r = int(ranks[n])
         if r < qs[n].shape[1]:
-            u, _ = leading_left_singular_vectors(unfold(g, n), r)
-            qs[n] = qs[n] @ u
-            g = ttm(g, u.T, n)
+            us[n], _ = leading_left_singular_vectors(unfold(g, n), r)
+    for n in range(d):
+        if us[n] is not None:
+            qs[n] = qs[n] @ us[n]
+            g = ttm(g, us[n].T, n)
     err = tucker_error(x, g, qs, chunk) if with_error else None
     return qs, g, err, ys
 

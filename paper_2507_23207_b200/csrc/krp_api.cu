@@ -347,8 +347,8 @@ static int rhosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_t
   }();
   float* G0 = ar.take<float>(coreR);  // R^d core
   float* G1 = ar.take<float>(coreR);
-  double* H = ar.take<double>(static_cast<size_t>(R) * R);
-  float* U = ar.take<float>(static_cast<size_t>(R) * R);
+  double* H = ar.take<double>(static_cast<size_t>(d) * R * R);  // one Gram per mode (HOSVD of the core)
+  float* U = ar.take<float>(static_cast<size_t>(d) * R * R);
   int rdims_all[kMaxD];
   for (int k = 0; k < d; ++k) rdims_all[k] = R;
   const int64_t cmax = chain_max(g, rdims_all);
@@ -424,22 +424,39 @@ static int rhosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_t
   if (dist) ops[d - 1].A = Qfull[d - 1] + slab_begin * R;
   KRP_TRY(ttm_chain(X, g, ops, CA, CB, G0, s));
   if (dist) KRP_TRY(allreduce_sum_f32(dc, G0, static_cast<size_t>(coreR), s));
-  // ---- 4. truncation R -> r_n by HOSVD of the small core (reading R4)
+  // ---- 4. truncation R -> r_n by HOSVD of the small core (reading R4): every U_n comes from the
+  //      untruncated core G0, so the d Gram matrices and eigenproblems are independent (one batched
+  //      eigensolver launch); then G = G0 x_1 U_1^T ... x_d U_d^T and Q_n <- Qfull_n U_n
   int64_t cd[kMaxD];
   for (int k = 0; k < d; ++k) cd[k] = R;
+  const Dims c0g = make_dims(d, cd);
+  const double* Hk[kMaxD];
+  float* Uk[kMaxD];
+  int rk[kMaxD];
+  int neig = 0;
+  for (int k = 0; k < d; ++k) {
+    if (ranks[k] < R) {
+      double* Hm = H + static_cast<size_t>(k) * R * R;
+      KRP_TRY(mode_gram(G0, c0g, k, Hm, ar, s));
+      ar.off = scratch_mark;
+      Hk[neig] = Hm;
+      Uk[neig] = U + static_cast<size_t>(k) * R * R;
+      rk[neig] = ranks[k];
+      ++neig;
+    }
+  }
+  if (neig > 0) KRP_TRY(sym_eig_top_batched(Hk, neig, R, rk, Uk, s));
   float* Gc = G0;
   float* Gn = G1;
   for (int k = 0; k < d; ++k) {
     const Dims cg = make_dims(d, cd);
     if (ranks[k] < R) {
-      KRP_TRY(mode_gram(Gc, cg, k, H, ar, s));
-      ar.off = scratch_mark;
-      KRP_TRY(sym_eig_top(H, R, ranks[k], U, s));
+      const float* Um = U + static_cast<size_t>(k) * R * R;
       // Q_k <- Qfull_k U  (Qfull as dims (R, I_k): mode-0 TTM with A = U^T, (j,i) at U[i*r + j])
       int64_t qd[2] = {R, gd[k]};
-      KRP_TRY(ttm(Qfull[k], make_dims(2, qd), 0, U, ranks[k], 1, ranks[k], Q[k], s));
+      KRP_TRY(ttm(Qfull[k], make_dims(2, qd), 0, Um, ranks[k], 1, ranks[k], Q[k], s));
       // G <- G x_k U^T
-      KRP_TRY(ttm(Gc, cg, k, U, ranks[k], 1, ranks[k], Gn, s));
+      KRP_TRY(ttm(Gc, cg, k, Um, ranks[k], 1, ranks[k], Gn, s));
       std::swap(Gc, Gn);
       cd[k] = ranks[k];
     } else {

@@ -39,6 +39,8 @@ int mode_gram(const float* T, const Dims& g, int n, double* H, Arena& ar, cudaSt
 // Leading r eigenvectors (descending eigenvalues) of a symmetric J x J fp64 matrix (J <= 64),
 // written as U (J x r row-major) in fp32.
 int sym_eig_top(const double* H, int J, int r, float* U, cudaStream_t s);
+// count independent problems in one launch (one block each): H[k] (J x J) -> U[k] (J x r[k])
+int sym_eig_top_batched(const double* const* H, int count, int J, const int* r, float* const* U, cudaStream_t s);
 
 // sum (X - Xh)^2 and sum X^2 over n elements, fp64, fixed order; out[0], out[1] accumulate (+=).
 size_t sqdiff_ws_bytes(int64_t n);

@@ -156,7 +156,8 @@ __global__ void apply_linv_kernel(const T* __restrict__ Y, int64_t rows, int R, 
   if (Qf) Qf[idx] = static_cast<float>(s);
 }
 
-__global__ void jacobi_top_kernel(const double* __restrict__ Hm, int J, int r, float* __restrict__ U);
+struct EigBatch;
+__global__ void jacobi_top_kernel(EigBatch batch, int J);
 constexpr size_t kSquareSmem = 2 * kGramMaxR * (kGramMaxR + 1) * sizeof(double);
 constexpr size_t kJacobiSmem = 3 * kGramMaxR * (kGramMaxR + 1) * sizeof(double);
 int set_square_smem_attrs() {
@@ -486,15 +487,26 @@ __device__ __forceinline__ void jacobi_rot(const double (*A)[kGramMaxR + 1], int
   c = 1.0;
   s = 0.0;
   if (q < J && A[p][q] != 0.0) {
-    const double tau = (A[q][q] - A[p][p]) / (2.0 * A[p][q]);
-    const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-    c = rsqrt(1.0 + t * t);
+    // t = sign(tau) / (|tau| + sqrt(1 + tau^2)) with tau = x / y, x = a_qq - a_pp, y = 2 a_pq, written
+    // with one divide: t = sign(x) y / (|x| + sqrt(x^2 + y^2))  (sign(0) = +1)
+    const double x = A[q][q] - A[p][p], y = 2.0 * A[p][q];
+    const double t = (x >= 0.0 ? y : -y) / (fabs(x) + sqrt(fma(x, x, y * y)));
+    c = rsqrt(fma(t, t, 1.0));
     s = t * c;
   }
 }
 
-__global__ void __launch_bounds__(1024) jacobi_top_kernel(const double* __restrict__ Hm, int J, int r,
-                                                          float* __restrict__ U) {
+struct EigBatch {
+  const double* H[kMaxD];
+  float* U[kMaxD];
+  int r[kMaxD];
+};
+
+// one problem per block: blockIdx.x selects (H, r, U) of the batch
+__global__ void __launch_bounds__(1024) jacobi_top_kernel(EigBatch batch, int J) {
+  const double* __restrict__ Hm = batch.H[blockIdx.x];
+  float* __restrict__ U = batch.U[blockIdx.x];
+  const int r = batch.r[blockIdx.x];
   extern __shared__ double dyn_smem[];
   typedef double Row[kGramMaxR + 1];
   Row* Abuf[2] = {reinterpret_cast<Row*>(dyn_smem), reinterpret_cast<Row*>(dyn_smem + kGramMaxR * (kGramMaxR + 1))};
@@ -764,15 +776,29 @@ int mode_gram(const float* T, const Dims& g, int n, double* H, Arena& ar, cudaSt
   return KRP_OK;
 }
 
-int sym_eig_top(const double* H, int J, int r, float* U, cudaStream_t s) {
-  if (J > kGramMaxR || r > J) {
-    set_error("eigensolver: J=%d r=%d unsupported", J, r);
+int sym_eig_top_batched(const double* const* H, int count, int J, const int* r, float* const* U, cudaStream_t s) {
+  if (count < 1 || count > kMaxD || J > kGramMaxR) {
+    set_error("eigensolver: count=%d J=%d unsupported", count, J);
     return KRP_EINVAL;
   }
+  EigBatch b{};
+  for (int k = 0; k < count; ++k) {
+    if (r[k] > J || r[k] < 0) {
+      set_error("eigensolver: J=%d r=%d unsupported", J, r[k]);
+      return KRP_EINVAL;
+    }
+    b.H[k] = H[k];
+    b.U[k] = U[k];
+    b.r[k] = r[k];
+  }
   KRP_TRY(set_square_smem_attrs());
-  jacobi_top_kernel<<<1, 1024, kJacobiSmem, s>>>(H, J, r, U);
+  jacobi_top_kernel<<<count, 1024, kJacobiSmem, s>>>(b, J);
   KRP_CHECK_LAUNCH();
   return KRP_OK;
+}
+
+int sym_eig_top(const double* H, int J, int r, float* U, cudaStream_t s) {
+  return sym_eig_top_batched(&H, 1, J, &r, &U, s);
 }
 
 size_t sqdiff_ws_bytes(int64_t n) { return align_up(2 * 1184 * sizeof(double), 256); }

@@ -333,6 +333,29 @@ def test_rhosvd_error_bounds():
         assert q.shape[1] == r and np.allclose(q.T @ q, np.eye(r), atol=1e-12)
 
 
+def test_rhosvd_truncation_is_hosvd_of_the_core():
+    """Reading R4 ("hosvd on the core"): every U_n = Qfull_nᵀ Q_n diagonalises the mode-n Gram of the
+    UNTRUNCATED core G0 with its r_n largest eigenvalues (checked with a symmetric eigen-solver, not the
+    oracle's SVD); a sequential (ST) truncation of the core fails this for the second truncated mode."""
+    dims, R, ranks = (14, 12, 10), 6, (3, 4, 6)
+    x = _rand_tensor_with_decay(dims, 52)
+    om = _rand_omegas(dims, R, 53)
+    qs, g, _, ys = oracle.rhosvd(x, om, ranks)
+    qf = [oracle.thin_qr(y)[0] for y in ys]
+    g0 = oracle.multi_ttm(x, [q.T for q in qf])
+    for n, r in enumerate(ranks):
+        if r == R:
+            assert np.allclose(qs[n], qf[n], atol=1e-13)
+            continue
+        u = qf[n].T @ qs[n]
+        h = oracle.unfold(g0, n) @ oracle.unfold(g0, n).T
+        ev = np.linalg.eigvalsh(h)[::-1][:r]
+        m = u.T @ h @ u
+        assert np.allclose(np.diag(m), ev, rtol=1e-10, atol=1e-12 * ev[0])
+        assert np.abs(m - np.diag(np.diag(m))).max() < 1e-10 * ev[0]
+    assert np.allclose(g, oracle.multi_ttm(g0, [(qf[n].T @ qs[n]).T for n in range(3)]), atol=1e-12)
+
+
 def test_ranks_equal_dims_exact():
     """ranks = dims (sketch width = every mode size) -> exact reconstruction."""
     dims = (5, 5, 5)
