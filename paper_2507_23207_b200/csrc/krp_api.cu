@@ -229,6 +229,37 @@ static int ttm_chain(const float* X, Dims g, const TtmOp* ops, float* bufA, floa
 // Orchestrates RHOSVD for a (possibly sharded) tensor.  When comm != nullptr, the local core and
 // the error sums are all-reduced across ranks (slab sharding along the last mode; Y is global).
 struct DistCtx;
+// Per-device side streams for independent per-mode work (the d CholeskyQR2 factorisations of rHOSVD):
+// forked from and joined back into the caller's stream with events, so the caller sees one ordered
+// stream (and a captured graph gets parallel branches).
+struct SideStreams {
+  cudaStream_t st[kMaxD];
+  cudaEvent_t fork, join[kMaxD];
+  bool ok = false;
+};
+static std::mutex g_side_mu;
+static int side_streams(SideStreams** out) {
+  static SideStreams per_dev[64];
+  int dev = 0;
+  KRP_CHECK_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) {
+    set_error("device ordinal %d out of range", dev);
+    return KRP_EINVAL;
+  }
+  std::lock_guard<std::mutex> lk(g_side_mu);
+  SideStreams& ss = per_dev[dev];
+  if (!ss.ok) {
+    for (int k = 0; k < kMaxD; ++k) {
+      KRP_CHECK_CUDA(cudaStreamCreateWithFlags(&ss.st[k], cudaStreamNonBlocking));
+      KRP_CHECK_CUDA(cudaEventCreateWithFlags(&ss.join[k], cudaEventDisableTiming));
+    }
+    KRP_CHECK_CUDA(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
+    ss.ok = true;
+  }
+  *out = &ss;
+  return KRP_OK;
+}
+
 static int allreduce_sum_f32(DistCtx* c, float* buf, size_t count, cudaStream_t s);
 static int allreduce_sum_f64(DistCtx* c, double* buf, size_t count, cudaStream_t s);
 
@@ -359,7 +390,11 @@ static int rhosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_t
   bool want[kMaxD];
   for (int k = 0; k < d; ++k) want[k] = true;
   size_t scratch = sketch_ws_bytes(g, R, want);
-  for (int k = 0; k < d; ++k) scratch = std::max(scratch, cholqr_ws_bytes(gd[k], R));
+  {  // the d CholeskyQR2 run concurrently: disjoint scratch per mode
+    size_t qr = 0;
+    for (int k = 0; k < d; ++k) qr += cholqr_ws_bytes(gd[k], R);
+    scratch = std::max(scratch, qr);
+  }
   {
     int64_t cd[kMaxD];
     for (int k = 0; k < d; ++k) cd[k] = R;
@@ -413,9 +448,21 @@ static int rhosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_t
   ar.off = scratch_mark;
   // ---- multi-GPU: one all-reduce(sum) of the packed sketches (the zero-padded Y_d doubles as the gather)
   if (dist) KRP_TRY(allreduce_sum_f32(dc, Ypack, static_cast<size_t>(ysum), s));
-  // ---- 2. thin QR of every Y_n, replicated
-  for (int k = 0; k < d; ++k) {
-    KRP_TRY(cholqr(Ybuf[k], gd[k], R, Qfull[k], nullptr, flag, ar, s));
+  // ---- 2. thin QR of every Y_n, replicated; the d factorisations are independent and run on
+  //      side streams (each is a chain of small latency-bound kernels)
+  {
+    SideStreams* ss = nullptr;
+    KRP_TRY(side_streams(&ss));
+    KRP_CHECK_CUDA(cudaEventRecord(ss->fork, s));
+    size_t off = scratch_mark;
+    for (int k = 0; k < d; ++k) {
+      KRP_CHECK_CUDA(cudaStreamWaitEvent(ss->st[k], ss->fork, 0));
+      ar.off = off;
+      KRP_TRY(cholqr(Ybuf[k], gd[k], R, Qfull[k], nullptr, flag, ar, ss->st[k]));
+      off += cholqr_ws_bytes(gd[k], R);
+      KRP_CHECK_CUDA(cudaEventRecord(ss->join[k], ss->st[k]));
+      KRP_CHECK_CUDA(cudaStreamWaitEvent(s, ss->join[k], 0));
+    }
     ar.off = scratch_mark;
   }
   // ---- 3. core G = X x_1 Q_1^T ... x_d Q_d^T on the local slab, then all-reduce

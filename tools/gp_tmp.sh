@@ -1,4 +1,4 @@
-T=gpurun_out/rh7
+T=gpurun_out/rh8
 mkdir -p $T
 {
 for c in c2 c3 c4 c5; do
