@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(256) ttm_kernel(const float* __restrict__ X, i
   }
 }
 
-// Mode-0 TTM (L == 1, I % 4 == 0, 16-byte aligned X, J <= 64): Y[j + J*h] = sum_i A[j*sj + i*si] X[i + I*h],
+// Mode-0 TTM (L == 1, I % 4 == 0, 16-byte aligned X, J <= 40): Y[j + J*h] = sum_i A[j*sj + i*si] X[i + I*h],
 // i.e. the GEMM Y = A X with X column-major (each column h is I contiguous floats).  Block = 256 columns
 // h x all J rows; i in steps of 32 loaded as float4 (8 lanes cover one 128-byte column segment) and
 // transposed into Xs[i][h] (row stride 257: conflict-free stores and loads); warp ty owns rows
@@ -392,6 +392,125 @@ int launch_ttm_mode0(const float* X, int64_t I, int64_t H, const float* A, int J
   }
   const unsigned nb = static_cast<unsigned>((H + kM0Cols - 1) / kM0Cols);
   ttm_mode0_kernel<NB><<<nb, 256, smem, s>>>(X, I, H, A, J, sj, si, Y);
+  KRP_CHECK_LAUNCH();
+  return KRP_OK;
+}
+
+constexpr int kWCols = 512, kWK = 16, kWXP = kWCols, kWYP = kWCols + 4;
+template <int NB4>
+__global__ void __launch_bounds__(256, 1) ttm_mode0w_kernel(const float* __restrict__ X, int64_t I,
+                                                                           int64_t H, const float* __restrict__ A,
+                                                                           int J, int64_t sj, int64_t si,
+                                                                           float* __restrict__ Y) {
+  extern __shared__ __align__(16) float m0w[];
+  float* Xs = m0w;                 // [kWK][kWXP]
+  float* As = m0w + kWK * kWXP;  // [kWK][64]: row ii, slot jg*32 + b
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int jg = warp & 1, hg = warp >> 1;
+  const int NB = (J + 1) >> 1;
+  const int64_t h0 = static_cast<int64_t>(blockIdx.x) * kWCols;
+  // X loads: float4 f = tid + 256 k (k < 8): i quarter q = f & 3, column hl = f >> 2 = (tid >> 2) + 64 k, so
+  // 4 lanes read one column's 64 contiguous bytes (coalesced); stored transposed with the column index
+  // XOR-swizzled by 8 q (conflict-free stores, and float4 reads stay contiguous)
+  const int lq = tid & 3;
+  const int64_t hbase = h0 + (tid >> 2);
+  const float* xcol0 = X + hbase * I + 4 * lq;
+  const int64_t col64 = 64 * I;
+  const int64_t nv64 = H > hbase ? (H - hbase + 63) / 64 : 0;
+  const int nvalid = nv64 < 8 ? static_cast<int>(nv64) : 8;
+  float4 xr[8];
+  float ar[4];
+  auto fetch = [&](int64_t i0) {
+    const float* xp = xcol0 + i0;
+    const bool iin = i0 + 4 * lq < I;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      xr[k] = (iin && k < nvalid) ? __ldg(reinterpret_cast<const float4*>(xp)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      xp += col64;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {  // A slot e = tid + 256 k: ii = e >> 6, (jg', b) = e & 63
+      const int e = tid + 256 * k, ii = e >> 6, slot = e & 63, g = slot >> 5, b = slot & 31;
+      const int j = g * NB + b;
+      const int64_t i = i0 + ii;
+      ar[k] = (b < NB && j < J && i < I) ? __ldg(A + j * sj + i * si) : 0.f;
+    }
+  };
+  float acc[4][NB4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int b = 0; b < NB4; ++b) acc[c][b] = 0.f;
+  fetch(0);
+  const int xcol = hg * 128 + 4 * lane;
+  const float* as_row = As + jg * 32;
+  for (int64_t i0 = 0; i0 < I; i0 += kWK) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int hl = ((tid >> 2) + 64 * k) ^ (8 * lq);
+      Xs[(4 * lq + 0) * kWXP + hl] = xr[k].x;
+      Xs[(4 * lq + 1) * kWXP + hl] = xr[k].y;
+      Xs[(4 * lq + 2) * kWXP + hl] = xr[k].z;
+      Xs[(4 * lq + 3) * kWXP + hl] = xr[k].w;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) As[tid + 256 * k] = ar[k];
+    __syncthreads();
+    if (i0 + kWK < I) fetch(i0 + kWK);
+#pragma unroll 2
+    for (int ii = 0; ii < kWK; ++ii) {
+      const float4 xv = *reinterpret_cast<const float4*>(Xs + ii * kWXP + (xcol ^ (8 * ((ii >> 2) & 3))));
+#pragma unroll
+      for (int b4 = 0; b4 < NB4; b4 += 4) {
+        const float4 av = *reinterpret_cast<const float4*>(as_row + ii * 64 + b4);
+        const float a4[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          acc[0][b4 + u] = fmaf(xv.x, a4[u], acc[0][b4 + u]);
+          acc[1][b4 + u] = fmaf(xv.y, a4[u], acc[1][b4 + u]);
+          acc[2][b4 + u] = fmaf(xv.z, a4[u], acc[2][b4 + u]);
+          acc[3][b4 + u] = fmaf(xv.w, a4[u], acc[3][b4 + u]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // stage Ys[j][h] (float4 over the thread's 4 columns) and write the contiguous output range
+  float* Ys = m0w;
+#pragma unroll
+  for (int b = 0; b < NB4; ++b) {
+    const int j = jg * NB + b;
+    if (b < NB && j < J)
+      *reinterpret_cast<float4*>(Ys + j * kWYP + hg * 128 + 4 * lane) =
+          make_float4(acc[0][b], acc[1][b], acc[2][b], acc[3][b]);
+  }
+  __syncthreads();
+  const int64_t ncols = min(static_cast<int64_t>(kWCols), H - h0);
+  const int total = static_cast<int>(ncols) * J;
+  float* out = Y + h0 * J;
+  for (int e = tid; e < total; e += 256) {
+    const int h = e / J, j = e - h * J;
+    out[e] = Ys[j * kWYP + h];
+  }
+}
+
+size_t ttm_mode0w_smem(int J) {
+  const size_t tiles = (static_cast<size_t>(kWK) * kWXP + kWK * 64) * sizeof(float);
+  const size_t out = static_cast<size_t>(J) * kWYP * sizeof(float);
+  return tiles > out ? tiles : out;
+}
+
+template <int NB4>
+int launch_ttm_mode0w(const float* X, int64_t I, int64_t H, const float* A, int J, int64_t sj, int64_t si, float* Y,
+                     cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    KRP_CHECK_CUDA(cudaFuncSetAttribute(ttm_mode0w_kernel<NB4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(ttm_mode0w_smem(64))));
+    attr = true;
+  }
+  const unsigned nb = static_cast<unsigned>((H + kWCols - 1) / kWCols);
+  ttm_mode0w_kernel<NB4><<<nb, 256, ttm_mode0w_smem(J), s>>>(X, I, H, A, J, sj, si, Y);
   KRP_CHECK_LAUNCH();
   return KRP_OK;
 }
@@ -728,16 +847,16 @@ int ttm(const float* X, const Dims& g, int n, const float* A, int J, int64_t sj,
   const int64_t L = g.stride[n], I = g.n[n], H = g.N / (L * I);
   const int64_t P = L * H;
   if (P == 0 || J == 0) return KRP_OK;
-  if (L == 1 && J <= 64 && I % 4 == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 && H >= 148 * kM0Cols / 4) {
+  if (L == 1 && J <= 64 && I % 4 == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 && H >= 148 * kM0Cols / 8) {
     switch ((J + 7) / 8) {
       case 1: return launch_ttm_mode0<1>(X, I, H, A, J, sj, si, Y, s);
       case 2: return launch_ttm_mode0<2>(X, I, H, A, J, sj, si, Y, s);
       case 3: return launch_ttm_mode0<3>(X, I, H, A, J, sj, si, Y, s);
       case 4: return launch_ttm_mode0<4>(X, I, H, A, J, sj, si, Y, s);
       case 5: return launch_ttm_mode0<5>(X, I, H, A, J, sj, si, Y, s);
-      case 6: return launch_ttm_mode0<6>(X, I, H, A, J, sj, si, Y, s);
-      case 7: return launch_ttm_mode0<7>(X, I, H, A, J, sj, si, Y, s);
-      default: return launch_ttm_mode0<8>(X, I, H, A, J, sj, si, Y, s);
+      case 6: return launch_ttm_mode0w<24>(X, I, H, A, J, sj, si, Y, s);
+      case 7: return launch_ttm_mode0w<28>(X, I, H, A, J, sj, si, Y, s);
+      default: return launch_ttm_mode0w<32>(X, I, H, A, J, sj, si, Y, s);
     }
   }
   const unsigned nb = static_cast<unsigned>((P + 63) / 64);

@@ -151,7 +151,9 @@ def _check_factors(Q, ranks):
                                         # mode-0 TTM kernel with ragged i (100 % 32) and column (10500 % 256) tails
                                         ("c2", (100, 150, 70)),
                                         # I_1 % 4 != 0: the generic TTM path for the large first contraction
-                                        ("c2", (99, 120, 90))])
+                                        ("c2", (99, 120, 90)),
+                                        # wide (J = 60) mode-0 TTM kernel with ragged i and column tails
+                                        ("c5", (100, 130, 90))])
 def test_rhosvd_parity(krp, name, small):
     cfg = synth.config(name) if small is None else synth.config(name).scaled(small)
     x = synth.tensor(cfg, 0)
