@@ -55,6 +55,11 @@ def test_argument_validation_without_device(krp):
     # R out of range
     assert lib.krp_sketch_all_modes(1, 3, dims, ptrs, 0, ptrs, None, 0, None) == 1
     assert lib.krp_sketch_all_modes(1, 3, dims, ptrs, 129, ptrs, None, 0, None) == 1
+    # empty mode (a dimension of size 0) and negative sizes are rejected before any launch
+    for bad_dims in ((8, 0, 8), (0, 8, 8), (8, 8, -1)):
+        dz = (ctypes.c_int64 * 3)(*bad_dims)
+        assert lib.krp_sketch_all_modes(1, 3, dz, ptrs, 4, ptrs, None, 0, None) == 1
+        assert b"dims" in lib.krp_last_error_message()
     # null omega entry
     bad = (ctypes.c_void_p * 3)(1, None, 1)
     assert lib.krp_sketch_all_modes(1, 3, dims, bad, 4, ptrs, None, 0, None) == 1

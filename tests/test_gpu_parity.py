@@ -71,6 +71,8 @@ SHAPES = [
     ((256, 129, 3), 16), ((128, 128, 40), 40), ((256, 256, 17), 40), ((384, 128, 9), 64),
     ((16, 16, 16, 16, 16), 20), ((64, 64, 8, 8), 20), ((6, 5, 4, 3, 2, 2), 6), ((1000, 3), 2),
     ((128, 256, 7), 128), ((512, 128, 5), 30),
+    # degenerate cases: R = 1, unit modes (first, middle, last), a single-element tensor
+    ((128, 128, 128), 1), ((1, 128, 256), 8), ((128, 1, 256), 8), ((256, 128, 1), 8), ((1, 1, 1), 1),
 ]
 
 
