@@ -369,7 +369,7 @@ static int rhosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_t
     }
   }
   for (int k = 0; k < d; ++k) Qfull[k] = ar.take<float>(gd[k] * R);
-  int* flag = ar.take<int>(4);
+  int* flag = ar.take<int>(kMaxD);  // one CholeskyQR status word per mode (the chains run concurrently)
   double* errsum = ar.take<double>(2);
   const int64_t coreR = [&] {
     int64_t c = 1;
@@ -434,7 +434,7 @@ static int rhosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_t
   }
   ar.off = scratch_mark;
 
-  KRP_CHECK_CUDA(cudaMemsetAsync(flag, 0, 4 * sizeof(int), s));
+  KRP_CHECK_CUDA(cudaMemsetAsync(flag, 0, kMaxD * sizeof(int), s));
   // ---- 1. memoized all-mode sketch of the local slab (Alg. 7 line 3 with memoization)
   OmegaPtrs om = make_om(omega, d, -1);
   if (dist) om.p[d - 1] = omega[d - 1] + slab_begin * R;  // local rows of the global Omega_d
@@ -458,7 +458,7 @@ static int rhosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_t
     for (int k = 0; k < d; ++k) {
       KRP_CHECK_CUDA(cudaStreamWaitEvent(ss->st[k], ss->fork, 0));
       ar.off = off;
-      KRP_TRY(cholqr(Ybuf[k], gd[k], R, Qfull[k], nullptr, flag, ar, ss->st[k]));
+      KRP_TRY(cholqr(Ybuf[k], gd[k], R, Qfull[k], nullptr, flag + k, ar, ss->st[k]));
       off += cholqr_ws_bytes(gd[k], R);
       KRP_CHECK_CUDA(cudaEventRecord(ss->join[k], ss->st[k]));
       KRP_CHECK_CUDA(cudaStreamWaitEvent(s, ss->join[k], 0));
@@ -538,12 +538,14 @@ static int rhosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_t
     if (dist) KRP_TRY(allreduce_sum_f64(dc, errsum, 2, s));
   }
   // ---- status
-  int hflag[4] = {0, 0, 0, 0};
+  int hflag[kMaxD] = {};
   double herr[2] = {0.0, 0.0};
   KRP_CHECK_CUDA(cudaMemcpyAsync(hflag, flag, sizeof(hflag), cudaMemcpyDeviceToHost, s));
   if (rel_err) KRP_CHECK_CUDA(cudaMemcpyAsync(herr, errsum, sizeof(herr), cudaMemcpyDeviceToHost, s));
   KRP_CHECK_CUDA(cudaStreamSynchronize(s));
-  if (hflag[0] & 2) {
+  int fl = 0;
+  for (int k = 0; k < d; ++k) fl |= hflag[k];
+  if (fl & 2) {
     set_error("CholeskyQR breakdown (shifted fallback failed)");
     return KRP_ENUMERIC;
   }

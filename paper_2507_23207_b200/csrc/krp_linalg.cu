@@ -22,7 +22,9 @@ constexpr int kGramMaxR = 64;
 // ------------------------------------------------------------------ Gram of a tall-skinny matrix
 template <typename T>
 __global__ void __launch_bounds__(256) gram_partial_kernel(const T* __restrict__ Y, int64_t rows, int R,
-                                                           int64_t rows_per_block, double* __restrict__ partial) {
+                                                           int64_t rows_per_block, double* __restrict__ partial,
+                                                           const int* __restrict__ gate = nullptr) {
+  if (gate && !(*gate & 1)) return;
   __shared__ double tile[32][kGramMaxR + 1];
   const int64_t r_begin = static_cast<int64_t>(blockIdx.x) * rows_per_block;
   const int64_t r_end = min(rows, r_begin + rows_per_block);
@@ -56,10 +58,11 @@ __global__ void __launch_bounds__(256) gram_partial_kernel(const T* __restrict__
   }
 }
 
+// gate (optional): run only if *gate & 1 (the shifted first CholeskyQR pass happened)
 __global__ void sum_partials_f64_kernel(const double* __restrict__ partial, int P, int64_t len,
-                                        double* __restrict__ out) {
+                                        double* __restrict__ out, const int* __restrict__ gate = nullptr) {
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= len) return;
+  if (idx >= len || (gate && !(*gate & 1))) return;
   double s = 0.0;
   for (int p = 0; p < P; ++p) s += partial[static_cast<int64_t>(p) * len + idx];
   out[idx] = s;
@@ -69,14 +72,22 @@ __global__ void sum_partials_f64_kernel(const double* __restrict__ partial, int 
 // G (R x R, fp64) = L L^T.  Writes Linv (R x R row-major, lower) so that Q = Y Linv^T.
 // allow_shift: on breakdown, retry with G + s I, s = 11 (rows R + R(R+1)) u ||Y||_F^2 (flag |= 1);
 // a breakdown that cannot be shifted sets flag |= 2.
-__global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict__ G, int R, int64_t rows,
-                                                        double* __restrict__ Linv_out, int* flag, int allow_shift) {
+// allow_shift == 2: the third (refinement) pass — factorise only if the first pass was shifted
+// (flag & 1), else write Linv = I so that the pass is an exact copy (plain CholeskyQR2).
+__global__ void __launch_bounds__(256) chol_inv_kernel(const double* __restrict__ G, int R, int64_t rows,
+                                                       double* __restrict__ Linv_out, int* flag, int allow_shift) {
+  if (allow_shift == 2 && !(*flag & 1)) {
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) Linv_out[e] = (e / R == e % R) ? 1.0 : 0.0;
+    return;
+  }
+  if (allow_shift == 2) allow_shift = 0;
   extern __shared__ double dyn_smem[];
   double(*A)[kGramMaxR + 1] = reinterpret_cast<double(*)[kGramMaxR + 1]>(dyn_smem);
   double(*Li)[kGramMaxR + 1] = reinterpret_cast<double(*)[kGramMaxR + 1]>(dyn_smem + kGramMaxR * (kGramMaxR + 1));
   __shared__ int fail;
   __shared__ double shift;
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x, nt = blockDim.x;  // 256 threads: a 16 x 16 grid for the rank-1 updates
+  const int tx = tid & 15, ty = tid >> 4;
   if (tid == 0) shift = 0.0;
   for (int attempt = 0; attempt < 2; ++attempt) {
     __syncthreads();
@@ -99,10 +110,10 @@ __global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict
       for (int i = j + 1 + tid; i < R; i += nt) A[i][j] /= ljj;
       if (tid == 0) A[j][j] = ljj;
       __syncthreads();
-      const int t = R - j - 1;  // trailing (i, k), j < k <= i < R, as a t x t square slot grid
-      for (int e = tid; e < t * t; e += nt) {
-        const int i = j + 1 + e / t, k = j + 1 + e % t;
-        if (k <= i) A[i][k] -= A[i][j] * A[k][j];
+      // trailing (i, k), j < k <= i < R, on a 16 x 16 thread grid (no integer division)
+      for (int i = j + 1 + ty; i < R; i += 16) {
+        const double lij = A[i][j];
+        for (int k = j + 1 + tx; k <= i; k += 16) A[i][k] -= lij * A[k][j];
       }
       __syncthreads();
     }
@@ -132,10 +143,9 @@ __global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict
     const double d = A[i][i];
     for (int c = tid; c <= i; c += nt) Li[i][c] /= d;
     __syncthreads();
-    const int t = R - i - 1;  // rows i+1..R-1, columns 0..i
-    for (int e = tid; e < t * (i + 1); e += nt) {
-      const int r = i + 1 + e / (i + 1), c = e % (i + 1);
-      Li[r][c] -= A[r][i] * Li[i][c];
+    for (int r = i + 1 + ty; r < R; r += 16) {  // rows i+1..R-1, columns 0..i
+      const double lri = A[r][i];
+      for (int c = tx; c <= i; c += 16) Li[r][c] -= lri * Li[i][c];
     }
     __syncthreads();
   }
@@ -188,12 +198,12 @@ GramPlan plan_gram(int64_t rows) {
 }
 
 template <typename T>
-int gram(const T* Y, int64_t rows, int R, double* G, double* partial, cudaStream_t s) {
+int gram(const T* Y, int64_t rows, int R, double* G, double* partial, cudaStream_t s, const int* gate = nullptr) {
   GramPlan gp = plan_gram(rows);
-  gram_partial_kernel<T><<<gp.P, 256, 0, s>>>(Y, rows, R, gp.rows_per_block, partial);
+  gram_partial_kernel<T><<<gp.P, 256, 0, s>>>(Y, rows, R, gp.rows_per_block, partial, gate);
   KRP_CHECK_LAUNCH();
   const int64_t len = static_cast<int64_t>(R) * R;
-  sum_partials_f64_kernel<<<static_cast<unsigned>((len + 255) / 256), 256, 0, s>>>(partial, gp.P, len, G);
+  sum_partials_f64_kernel<<<static_cast<unsigned>((len + 255) / 256), 256, 0, s>>>(partial, gp.P, len, G, gate);
   KRP_CHECK_LAUNCH();
   return KRP_OK;
 }
@@ -822,19 +832,20 @@ int cholqr(const float* Y, int64_t rows, int R, float* Qf, double* Qd, int* flag
   const unsigned nb = static_cast<unsigned>((tot + 255) / 256);
   // pass 1 (shift allowed)
   KRP_TRY(gram<float>(Y, rows, R, G, part, s));
-  chol_inv_kernel<<<1, 1024, kSquareSmem, s>>>(G, R, rows, Li, flag_dev, 1);
+  chol_inv_kernel<<<1, 256, kSquareSmem, s>>>(G, R, rows, Li, flag_dev, 1);
   KRP_CHECK_LAUNCH();
   apply_linv_kernel<float><<<nb, 256, 0, s>>>(Y, rows, R, Li, Q1, nullptr);
   KRP_CHECK_LAUNCH();
   // pass 2
   KRP_TRY(gram<double>(Q1, rows, R, G, part, s));
-  chol_inv_kernel<<<1, 1024, kSquareSmem, s>>>(G, R, rows, Li, flag_dev, 0);
+  chol_inv_kernel<<<1, 256, kSquareSmem, s>>>(G, R, rows, Li, flag_dev, 0);
   KRP_CHECK_LAUNCH();
   apply_linv_kernel<double><<<nb, 256, 0, s>>>(Q1, rows, R, Li, Q2, nullptr);
   KRP_CHECK_LAUNCH();
-  // pass 3 (restores orthogonality after a shifted first pass; a no-op refinement otherwise)
-  KRP_TRY(gram<double>(Q2, rows, R, G, part, s));
-  chol_inv_kernel<<<1, 1024, kSquareSmem, s>>>(G, R, rows, Li, flag_dev, 0);
+  // pass 3 (restores orthogonality after a shifted first pass; skipped on the device otherwise, so the
+  // unshifted case is plain CholeskyQR2 and the last apply is an exact copy through Linv = I)
+  KRP_TRY(gram<double>(Q2, rows, R, G, part, s, flag_dev));
+  chol_inv_kernel<<<1, 256, kSquareSmem, s>>>(G, R, rows, Li, flag_dev, 2);
   KRP_CHECK_LAUNCH();
   apply_linv_kernel<double><<<nb, 256, 0, s>>>(Q2, rows, R, Li, Qd, Qf);
   KRP_CHECK_LAUNCH();
