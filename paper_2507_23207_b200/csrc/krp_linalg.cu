@@ -526,53 +526,88 @@ int launch_ttm_mode0w(const float* X, int64_t I, int64_t H, const float* A, int 
 }
 
 // ------------------------------------------------------------------ mode-n Gram
-// H[a][b] = sum over fibers f=(l,h) of T[l + L(a + J h)] T[l + L(b + J h)]
+// H[a][b] = sum over fibers f=(l,h) of T[l + L(a + J h)] T[l + L(b + J h)], fp64.
+// Fibers come in chunks of 32, converted to fp64 once into shared memory.  Thread blk of a group owns the
+// 4 x 4 block (a in 4ta.., b in 4tb..) of H: per fiber it reads 4 + 4 doubles (two LDS.128 each; lanes of
+// a warp share ta, so the a-reads broadcast) for 16 DFMAs.  With J <= 44 several groups split each
+// chunk's fibers (fiber ff goes to group ff % G) and are summed in group order at the end, so the
+// result is deterministic for a given plan.
+constexpr int kMgPitch = kGramMaxR + 2;  // doubles; 16-byte aligned rows
 __global__ void __launch_bounds__(256) mode_gram_partial_kernel(const float* __restrict__ T, int64_t L, int J,
                                                                 int64_t H, int64_t fibers_per_block,
                                                                 double* __restrict__ partial) {
-  __shared__ float F[32][kGramMaxR + 1];
+  __shared__ __align__(16) double F[32][kMgPitch];
+  __shared__ double red[3 * 64 * 16];
+  const int tid = threadIdx.x;
+  const int nblk = (J + 3) >> 2, T2 = nblk * nblk;
+  int G = 256 / T2;
+  G = G < 1 ? 1 : (G > 4 ? 4 : G);
+  const int g = tid / T2, blk = tid - g * T2;
+  const bool active = g < G;
+  const int ta = blk / nblk, tb = blk - (blk / nblk) * nblk;
+  const int Jp = nblk * 4;
   const int64_t nf = L * H;
   const int64_t f_begin = static_cast<int64_t>(blockIdx.x) * fibers_per_block;
   const int64_t f_end = min(nf, f_begin + fibers_per_block);
-  const int npairs = J * J;
-  double acc[16];
+  double acc[4][4];
 #pragma unroll
-  for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
   for (int64_t fb = f_begin; fb < f_end; fb += 32) {
-    for (int e = threadIdx.x; e < 32 * J; e += blockDim.x) {
-      int ff, a;
-      if (L == 1) {
-        a = e % J;
-        ff = e / J;
-      } else {
-        ff = e % 32;
-        a = e / 32;
+    const int64_t rem = f_end - fb;
+    const int nff = rem < 32 ? static_cast<int>(rem) : 32;
+    if (L == 1) {  // the chunk is the contiguous range T[J fb, J (fb + nff))
+      const float* src = T + J * fb;
+      for (int e = tid; e < 32 * Jp; e += 256) {
+        const int ff = e / Jp, a = e - ff * Jp;
+        F[ff][a] = (ff < nff && a < J) ? static_cast<double>(__ldg(src + ff * J + a)) : 0.0;
       }
+    } else {  // ff = tid % 32 is fixed per thread: one (l, h) decomposition per chunk
+      const int ff = tid & 31;
       const int64_t f = fb + ff;
-      float v = 0.f;
-      if (f < f_end) {
-        const int64_t l = f % L, h = f / L;
-        v = __ldg(T + l + L * (a + static_cast<int64_t>(J) * h));
-      }
-      F[ff][a] = v;
+      const int64_t l = f % L, h = f / L;
+      const float* src = T + l + L * J * h;
+      for (int a = tid >> 5; a < Jp; a += 8)
+        F[ff][a] = (ff < nff && a < J) ? static_cast<double>(__ldg(src + L * a)) : 0.0;
     }
     __syncthreads();
+    if (active) {
+      for (int ff = g; ff < nff; ff += G) {
+        const double2 a01 = *reinterpret_cast<const double2*>(&F[ff][4 * ta]);
+        const double2 a23 = *reinterpret_cast<const double2*>(&F[ff][4 * ta + 2]);
+        const double2 b01 = *reinterpret_cast<const double2*>(&F[ff][4 * tb]);
+        const double2 b23 = *reinterpret_cast<const double2*>(&F[ff][4 * tb + 2]);
+        const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+        const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int pidx = threadIdx.x + q * 256;
-      if (pidx < npairs) {
-        const int a = pidx / J, b = pidx % J;
-        double s = 0.0;
-        for (int ff = 0; ff < 32; ++ff) s = fma(static_cast<double>(F[ff][a]), static_cast<double>(F[ff][b]), s);
-        acc[q] += s;
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
       }
     }
     __syncthreads();
   }
+  if (active && g > 0)
 #pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    const int pidx = threadIdx.x + q * 256;
-    if (pidx < npairs) partial[static_cast<int64_t>(blockIdx.x) * npairs + pidx] = acc[q];
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) red[((g - 1) * T2 + blk) * 16 + i * 4 + j] = acc[i][j];
+  __syncthreads();
+  if (active && g == 0) {
+    for (int gg = 1; gg < G; ++gg)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] += red[((gg - 1) * T2 + blk) * 16 + i * 4 + j];
+    double* out = partial + static_cast<int64_t>(blockIdx.x) * J * J;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int ra = 4 * ta + i, cb = 4 * tb + j;
+        if (ra < J && cb < J) out[ra * J + cb] = acc[i][j];
+      }
   }
 }
 
