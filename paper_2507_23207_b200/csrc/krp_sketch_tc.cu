@@ -65,7 +65,7 @@ struct TcParams {
   int maxseg;  // max number of CTAs contributing to one (rb, cb) pair: partial slot = pair*maxseg + k
   int tm_acc, tm_chunk, tm_a;  // TMEM columns: accumulator stages, A-operand chunk stages, A1/A2
   uint32_t sm_x, sm_bp, sm_bq, sm_red, sm_bar, sm_ws;
-  float* partA1;  // [npairs*maxseg][128][R]
+  float* partA1;  // [npairs*maxseg][R][128]
   float* partA2;
   int* slot_pair;  // [nslot]
   float* Tpart;    // [RB*CB][S][R]
@@ -265,6 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
+  if (threadIdx.x == 0) KRP_TRACE(13, 56);  // (development timeline: kernel entry)
   if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
   if (threadIdx.x == 0) {
     for (int i = 0; i < p.NS; ++i) {
@@ -286,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  if (threadIdx.x == 0) KRP_TRACE(13, 57);  // prologue done
   pdl_launch_dependents();  // the assembly kernel may be scheduled now (it waits for this grid to finish)
 
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * p.T / gridDim.x;
@@ -533,6 +535,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // between the two sides.
     if (!(p.dbg & 16)) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsEpi));  // both epilogue WGs
     pdl_wait();  // B images and Ω_S rows come from the tables kernel launched just before
+    if (threadIdx.x == kEpiWarp0 * 32) KRP_TRACE(13, 58);  // tables visible
     const uint32_t ew = warp - kEpiWarp0;  // 0..7
     const uint32_t sub = warp & 3;         // TMEM lane quarter
     const bool pside = ew < 4;
@@ -574,12 +577,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int kslot = static_cast<int>(blockIdx.x - cta_of_tile(prev_pair * p.S, p.T, gridDim.x));
           const int64_t slot = prev_pair * p.maxseg + kslot;
           if (threadIdx.x == kEpiWarp0 * 32) p.slot_pair[slot] = static_cast<int>(prev_pair);
-          float* dst = (pside ? p.partA1 : p.partA2) + (slot * kTile + l) * R;
+          // slot layout [r][128]: for a fixed r the 32 lanes of a warp store 128 contiguous bytes
+          float* dst = (pside ? p.partA1 : p.partA2) + slot * kTile * R + l;
 
           if constexpr (RA > 0) {
 #pragma unroll
             for (int j = 0; j < RA; ++j) {
-              if (active && j < R) dst[j] = Areg[j];
+              if (active && j < R) dst[j * kTile] = Areg[j];
               Areg[j] = 0.f;
             }
           } else if (active) {
@@ -589,7 +593,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               tmem_ld_wait();
 #pragma unroll
               for (int j = 0; j < 8; ++j)
-                if (8 * rnd + j < R) dst[8 * rnd + j] = v[j];
+                if (8 * rnd + j < R) dst[(8 * rnd + j) * kTile] = v[j];
             }
           }
         }
@@ -609,12 +613,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           float4* dst = reinterpret_cast<float4*>(pside ? bq : bp);
           const int n4 = p.NP * 128 / 4;
           const int me = static_cast<int>(sub * 32 + lane);
-#pragma unroll 4
+#pragma unroll 8
           for (int i = me; i < n4; i += 128) dst[i] = __ldg(src + i);
         }
         fence_proxy_async_smem();
         named_bar_sync(1, kNumEpiWarps * 32);
         if (threadIdx.x == kEpiWarp0 * 32) mbar_arrive(b_ready);
+        if (threadIdx.x == kEpiWarp0 * 32 && seg == 0) KRP_TRACE(13, 59);  // first B images ready
         if (p.do_t) {  // W(lane, r) = hi + lo rows of the image just copied (B_Q for the P side, B_P for Q)
           const uint32_t lo_row = static_cast<uint32_t>(R8) * 128;
 #pragma unroll
@@ -704,12 +709,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int kslot = static_cast<int>(blockIdx.x - cta_of_tile(prev_pair * p.S, p.T, gridDim.x));
           const int64_t slot = prev_pair * p.maxseg + kslot;
           if (threadIdx.x == kEpiWarp0 * 32) p.slot_pair[slot] = static_cast<int>(prev_pair);
-          float* dst = (pside ? p.partA1 : p.partA2) + (slot * kTile + l) * R;
+          // slot layout [r][128]: for a fixed r the 32 lanes of a warp store 128 contiguous bytes
+          float* dst = (pside ? p.partA1 : p.partA2) + slot * kTile * R + l;
 
           if constexpr (RA > 0) {
 #pragma unroll
             for (int j = 0; j < RA; ++j) {
-              if (active && j < R) dst[j] = Areg[j];
+              if (active && j < R) dst[j * kTile] = Areg[j];
               Areg[j] = 0.f;
             }
           } else if (active) {
@@ -719,15 +725,17 @@ __global__ void __launch_bounds__(kThreads, 1)
               tmem_ld_wait();
 #pragma unroll
               for (int j = 0; j < 8; ++j)
-                if (8 * rnd + j < R) dst[8 * rnd + j] = v[j];
+                if (8 * rnd + j < R) dst[(8 * rnd + j) * kTile] = v[j];
             }
           }
         }
   }
+  if (threadIdx.x == kEpiWarp0 * 32) KRP_TRACE(13, 60);  // epilogue (incl. last flush) done
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == kMmaWarp) tmem_dealloc<512>(tbase);
+  if (threadIdx.x == 0) KRP_TRACE(13, 61);  // kernel end
 }
 
 // ------------------------------------------------------------------ Khatri-Rao tables
@@ -808,20 +816,21 @@ struct RedParams {
   float *outP, *outQ, *outT;  // non-null: the group is a single wanted mode, write its Y directly
 };
 
-// P(ρ,r) = Σ_{cb} Σ_{k < pnk[pair]} partA1[(rb*CB + cb)*maxseg + k][ρ%128][r]
+// P(ρ,r) = Σ_{cb} Σ_{k < pnk[pair]} partA1[(rb*CB + cb)*maxseg + k][r][ρ%128]
 // Qc(γ,r) likewise over rb;  Ts(s,r) = Σ_{pairs} Tpart[pair][s][r].
-// One block = 32 consecutive outputs (lanes, coalesced) x 8 warps; the flattened term list is split into
-// 8 contiguous shares, each summed in order with its loads issued 8 at a time, then warp 0 adds the 8
+// One block = 32 outputs x 8 warps: for P / Qc the 32 lanes take 32 consecutive rows ρ of one column r
+// (coalesced partial reads), for Ts 32 consecutive (s, r).  The flattened term list is split into 8
+// contiguous shares, each summed in order with its loads issued 8 at a time, then warp 0 adds the 8
 // shares in order: a fixed reduction tree (deterministic).  A block never straddles a 128-row block
-// (32 | 128*R) nor a region (regions are padded to whole blocks).  A group with a single mode IS that
-// mode's sketch, so its region is written straight into Y (outP / outQ / outT non-null).
+// (32 | 128) nor a region.  A group with a single mode IS that mode's sketch, so its region is written
+// straight into Y (outP / outQ / outT non-null).
 constexpr int kRedWarps = 8;
 __global__ void __launch_bounds__(256) tc_assemble_kernel(const __grid_constant__ RedParams p) {
   __shared__ float red[kRedWarps][32];
   pdl_wait();  // the partials are written by the sketch kernel
   const int w = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
   const int64_t nP = p.do_p ? p.M * p.R : 0, nQ = p.do_q ? p.C * p.R : 0, nT = p.do_t ? p.S * p.R : 0;
-  const int64_t bP = (nP + 31) / 32, bQ = (nQ + 31) / 32;
+  const int64_t bP = p.do_p ? (p.M + 31) / 32 * p.R : 0, bQ = p.do_q ? (p.C + 31) / 32 * p.R : 0;
   int64_t blk_id = blockIdx.x;
   int region;
   if (blk_id < bP) {
@@ -832,16 +841,19 @@ __global__ void __launch_bounds__(256) tc_assemble_kernel(const __grid_constant_
     blk_id -= bQ;
     region = 2;
   }
-  const int64_t idx = blk_id * 32 + lane;
+  int64_t idx = blk_id * 32 + lane;  // Ts: linear (s, r); P / Qc: replaced by rho * R + r below
+  bool valid = true;
   float acc = 0.f;
   if (region < 2) {
     const bool rows = region == 0;
-    const int64_t n = rows ? nP : nQ;
-    const uint32_t ic = static_cast<uint32_t>(idx < n ? idx : n - 1);
-    const uint32_t lin = ic / static_cast<uint32_t>(p.R);
-    const int r = static_cast<int>(ic - lin * static_cast<uint32_t>(p.R));
-    const int blk = static_cast<int>(lin / kTile), l = static_cast<int>(lin % kTile);
-    const float* part = (rows ? p.partA1 : p.partA2) + static_cast<int64_t>(l) * p.R + r;
+    const int64_t nrow = rows ? p.M : p.C;
+    const int r = static_cast<int>(blk_id % p.R);
+    const int64_t rho = (blk_id / p.R) * 32 + lane;
+    valid = rho < nrow;
+    const int64_t rc = valid ? rho : nrow - 1;
+    idx = rc * p.R + r;
+    const int blk = static_cast<int>(rc / kTile), l = static_cast<int>(rc % kTile);
+    const float* part = (rows ? p.partA1 : p.partA2) + static_cast<int64_t>(r) * kTile + l;
     const int64_t kstride = static_cast<int64_t>(kTile) * p.R;
     const int nother = rows ? p.CB : p.RB;
     const int64_t F = static_cast<int64_t>(nother) * p.maxseg;  // flattened (other block, slot) terms
@@ -886,12 +898,12 @@ __global__ void __launch_bounds__(256) tc_assemble_kernel(const __grid_constant_
     for (int i = 1; i < kRedWarps; ++i) tot += red[i][lane];
     const int64_t n = region == 0 ? nP : (region == 1 ? nQ : nT);
     float* out = region == 0 ? (p.outP ? p.outP : p.Pm) : (region == 1 ? (p.outQ ? p.outQ : p.Qc) : (p.outT ? p.outT : p.Ts));
-    if (idx < n) out[idx] = tot;
+    if (valid && idx < n) out[idx] = tot;
   }
 }
 
 int64_t assemble_blocks(int64_t M, int64_t C, int64_t S, int R, int do_p, int do_q, int do_t) {
-  return (do_p ? (M * R + 31) / 32 : 0) + (do_q ? (C * R + 31) / 32 : 0) + (do_t ? (S * R + 31) / 32 : 0);
+  return (do_p ? (M + 31) / 32 * R : 0) + (do_q ? (C + 31) / 32 * R : 0) + (do_t ? (S * R + 31) / 32 : 0);
 }
 
 struct TtvParams {

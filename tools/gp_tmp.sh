@@ -1,10 +1,6 @@
-T=gpurun_out/rh18
+T=gpurun_out/sw3
 mkdir -p $T
-{
-for c in c2 c3 c4; do
-  echo "== head"; KRP_LIB=abtest/libkrp_head.so timeout 120 python tools/rh_time.py $c 5
-  echo "== new";  timeout 120 python tools/rh_time.py $c 5
-done
-} > $T/log 2>&1
-timeout 1500 python -m pytest tests -m gpu -x -q -k "rhosvd or sthosvd or tucker or dist" > $T/pytest.log 2>&1
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:mode_gram -c 8 --csv --log-file $T/mg.csv python tools/rh_time.py c3 1 > $T/ncu.log 2>&1
+timeout 300 python tools/tc_sweep.py 512 40 > $T/sweep.log 2>&1
+for c in c2 c3 c4 c5; do timeout 120 python tools/tc_time.py $c 20 check; done > $T/time.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q > $T/pytest.log 2>&1
+timeout 300 python tools/slab_time.py c2 30 > $T/slab.log 2>&1
