@@ -142,7 +142,7 @@ __device__ __forceinline__ void epi_drain8(int rnd, float (&z)[8], uint32_t tD, 
   }
 }
 __device__ __forceinline__ void epi_math8(int rnd, const float (&z)[8], float (&acc)[8], const float* __restrict__ oms_g,
-                                          bool my_t, const float* w, uint32_t rbuf_s, int R8, uint32_t sub,
+                                          bool my_t, const float (&w)[8], uint32_t rbuf_s, int R8, uint32_t sub,
                                           uint32_t lane) {
   const int rr = 8 * rnd;
   float om[8], tv[8];
@@ -183,7 +183,7 @@ __device__ __forceinline__ void epi_math8(int rnd, const float (&z)[8], float (&
 }
 
 __device__ __forceinline__ void epi_round8(int rnd, float (&acc)[8], uint32_t tD, int R, int R8, int triple,
-                                           const float* __restrict__ oms_g, bool my_t, const float* w, uint32_t rbuf_s,
+                                           const float* __restrict__ oms_g, bool my_t, const float (&w)[8], uint32_t rbuf_s,
                                            uint32_t sub, uint32_t lane) {
   const int rr = 8 * rnd;
   float a[8], b[8], om[8], tv[8];
@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp >= kTmaWarp) {
   // producer warpgroup: one setmaxnreg for the whole group, then TMA / MMA / idle warps
-  if (!(p.dbg & 16)) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsProd));
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsProd));
   if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer
     if (elect_one()) {
@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // warps 8-11: P side (z1 -> A1 += z1·Ω_S), warps 12-15: Q side (z2 -> A2 += z2·Ω_S); A1/A2 live
     // in TMEM (lane = ρ resp. γ).  T(s,r) = Σ_ρ z1·W_L = Σ_γ z2·W_R: its 8-column rounds alternate
     // between the two sides.
-    if (!(p.dbg & 16)) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsEpi));  // both epilogue WGs
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsEpi));  // both epilogue WGs
     pdl_wait();  // B images and Ω_S rows come from the tables kernel launched just before
     if (threadIdx.x == kEpiWarp0 * 32) KRP_TRACE(13, 58);  // tables visible
     const uint32_t ew = warp - kEpiWarp0;  // 0..7
@@ -659,8 +659,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             epi_drain8(rnd, z8, tD, R, R8, p.triple);
 #pragma unroll
             for (int j = 0; j < 8; ++j) acc8[j] = Areg[8 * rnd + j];
+            float w8[8];  // register copy (no pointer into wreg, which must stay in registers)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) w8[j] = wreg[8 * (rnd >> 1) + j];
             if (!(p.dbg & 64))  // probe bit 64: drain only
-            epi_math8(rnd, z8, acc8, oms_g, p.do_t && !(p.dbg & 32) && ((rnd & 1) == (pside ? 0 : 1)), &wreg[8 * (rnd >> 1)], rbuf_s,
+            epi_math8(rnd, z8, acc8, oms_g, p.do_t && !(p.dbg & 32) && ((rnd & 1) == (pside ? 0 : 1)), w8, rbuf_s,
                       R8, sub, lane);
 #pragma unroll
             for (int j = 0; j < 8; ++j) Areg[8 * rnd + j] = acc8[j];
@@ -671,8 +674,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (rnd < nr) {
               float acc[8];
               tmem_ld8(tA + 8 * rnd, acc);
-              epi_round8(rnd, acc, tD, R, R8, p.triple, oms_g, p.do_t && ((rnd & 1) == (pside ? 0 : 1)),
-                         &wreg[8 * (rnd >> 1)], rbuf_s, sub, lane);
+              float w8[8];  // register copy (no pointer into wreg)
+#pragma unroll
+              for (int j = 0; j < 8; ++j) w8[j] = wreg[8 * (rnd >> 1) + j];
+              epi_round8(rnd, acc, tD, R, R8, p.triple, oms_g, p.do_t && ((rnd & 1) == (pside ? 0 : 1)), w8,
+                         rbuf_s, sub, lane);
               uint32_t accb[8];
 #pragma unroll
               for (int j = 0; j < 8; ++j) accb[j] = __float_as_uint(acc[j]);
