@@ -14,6 +14,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
          "-Xptxas", "-v"]
+if os.environ.get("KRP_DEV_TRACE"):  # development: compile the sketch kernel's role timeline in
+    FLAGS.append("-DKRP_DEV_TRACE")
 
 
 def _newest_input() -> float:

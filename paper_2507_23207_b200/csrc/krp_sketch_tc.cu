@@ -101,10 +101,18 @@ __host__ __device__ __forceinline__ int cta_of_tile(int64_t t, int64_t T, int gr
     else mbar_wait_spin((bar), (par));                               \
   } while (0)
 
+// Development timeline (CTA 0 role timestamps): compiled in only with -DKRP_DEV_TRACE, so the
+// production kernel carries no per-chunk trace checks.
+#ifdef KRP_DEV_TRACE
 #define KRP_TRACE(slot, idx)                                                                 \
   do {                                                                                       \
     if (p.trace && blockIdx.x == 0 && (idx) < 64) p.trace[(slot) * 64 + (idx)] = clock64(); \
   } while (0)
+#else
+#define KRP_TRACE(slot, idx) \
+  do {                       \
+  } while (0)
+#endif
 
 __device__ __forceinline__ uint32_t tf32_hi_bits(float x) { return __float_as_uint(x) & 0xFFFFE000u; }
 
