@@ -113,6 +113,17 @@ __host__ __device__ __forceinline__ int cta_of_tile(int64_t t, int64_t T, int gr
   do {                       \
   } while (0)
 #endif
+// Development probes (TcParams::dbg bits: disable TMA data / MMAs / epilogue math ...) and the
+// wait-mode switches exist only in KRP_DEV_TRACE builds; production always spins on the hot barriers.
+#ifdef KRP_DEV_TRACE
+#define KRP_DBG(bit) ((p.dbg & (bit)) != 0)
+#define KRP_MMA_SPIN (p.mma_spin != 0)
+#define KRP_SPLIT_SPIN (p.split_spin != 0)
+#else
+#define KRP_DBG(bit) false
+#define KRP_MMA_SPIN true
+#define KRP_SPLIT_SPIN true
+#endif
 
 __device__ __forceinline__ uint32_t tf32_hi_bits(float x) { return __float_as_uint(x) & 0xFFFFE000u; }
 
@@ -332,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (pf_t < t1) pf_issue();
         KWAIT(&empty_x[st], ph ^ 1);
         KRP_TRACE(0, t - t0);
-        if (p.dbg & 1) {  // probe: no data movement (the stage holds whatever it held)
+        if (KRP_DBG(1)) {  // probe: no data movement (the stage holds whatever it held)
           mbar_arrive(&full_x[st]);
         } else {
           mbar_arrive_expect_tx(&full_x[st], kStageFloats * 4);
@@ -375,14 +386,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         bph ^= 1;
         first = false;
       }
-      if (p.mma_spin) mbar_wait_spin(&acc_empty[ast], aph ^ 1); else KWAIT(&acc_empty[ast], aph ^ 1);
+      if (KRP_MMA_SPIN) mbar_wait_spin(&acc_empty[ast], aph ^ 1); else KWAIT(&acc_empty[ast], aph ^ 1);
       if (leader) KRP_TRACE(3, t - t0);
       tc_fence_after();
       const uint32_t dP = tbase + p.tm_acc + ast * 2 * p.DN;
       const uint32_t dQ = dP + p.DN;
         const uint64_t adesc_t = adesc0 + ((static_cast<uint64_t>(xst) * (kStageFloats * 4)) >> 4);
       for (int kc = 0; kc < nkc; ++kc) {
-        if (p.mma_spin) mbar_wait_spin(&chunk_full[cst], cph); else KWAIT(&chunk_full[cst], cph);
+        if (KRP_MMA_SPIN) mbar_wait_spin(&chunk_full[cst], cph); else KWAIT(&chunk_full[cst], cph);
         if (leader) KRP_TRACE(10, (t - t0) * 8 + kc);
         tc_fence_after();
         const uint32_t ach = tbase + p.tm_chunk + cst * 3 * CH;  // [P hi | P lo | Q lo]
@@ -390,7 +401,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t boff = static_cast<uint64_t>(kk0 >> 2) * katom_d + (kk0 & 3) * 2;
         // Q's A_hi: the raw tile in stage xst, box kk0/4 (16 KB), K offset (kk0 & 3) * 32 B
         const uint64_t aq = adesc_t + static_cast<uint64_t>(kk0 >> 2) * 1024 + (kk0 & 3) * 2;
-        if (leader && !(p.dbg & 2)) {  // probe bit 2: no MMAs (handshakes only)
+        if (leader && !KRP_DBG(2)) {  // probe bit 2: no MMAs (handshakes only)
           if (p.triple) {
 #pragma unroll
             for (int ks = 0; ks < CH / 8; ++ks) {
@@ -475,7 +486,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t stage_off = static_cast<uint32_t>(xst) * (kStageFloats * 4u);
       for (int kc = par; kc < nkc; kc += 2) {
         if (sub == 0 && lane == 0) KRP_TRACE(13, (t - t0) * 8 + kc);
-        if (p.split_spin) mbar_wait_spin(&chunk_ready[cst], cph ^ 1); else KWAIT(&chunk_ready[cst], cph ^ 1);
+        if (KRP_SPLIT_SPIN) mbar_wait_spin(&chunk_ready[cst], cph ^ 1); else KWAIT(&chunk_ready[cst], cph ^ 1);
         if (sub == 0 && lane == 0) KRP_TRACE(8, (t - t0) * 8 + kc);
         tc_fence_after();
         const uint32_t ch = tbase + lane_off + p.tm_chunk + cst * 3 * CH;
@@ -642,7 +653,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       KWAIT(&acc_full[ast], aph);
-      if (p.dbg & 4) {  // probe: no epilogue math
+      if (KRP_DBG(4)) {  // probe: no epilogue math
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[ast]);
@@ -670,8 +681,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             float w8[8];  // register copy (no pointer into wreg, which must stay in registers)
 #pragma unroll
             for (int j = 0; j < 8; ++j) w8[j] = wreg[8 * (rnd >> 1) + j];
-            if (!(p.dbg & 64))  // probe bit 64: drain only
-            epi_math8(rnd, z8, acc8, oms_g, p.do_t && !(p.dbg & 32) && ((rnd & 1) == (pside ? 0 : 1)), w8, rbuf_s,
+            if (!KRP_DBG(64))  // probe bit 64: drain only
+            epi_math8(rnd, z8, acc8, oms_g, p.do_t && !KRP_DBG(32) && ((rnd & 1) == (pside ? 0 : 1)), w8, rbuf_s,
                       R8, sub, lane);
 #pragma unroll
             for (int j = 0; j < 8; ++j) Areg[8 * rnd + j] = acc8[j];
@@ -705,7 +716,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ast = 0;
         aph ^= 1;
       }
-      if (p.do_t && !(p.dbg & 32)) {  // (probe bit 32: no T reduction)
+      if (p.do_t && !KRP_DBG(32)) {  // (probe bit 32: no T reduction)
         // fixed-order sum of the four lane quarters for every r (the two sides wrote disjoint rounds)
         named_bar_sync(2, kNumEpiWarps * 32);
         const int e = static_cast<int>(ew * 32 + lane);
