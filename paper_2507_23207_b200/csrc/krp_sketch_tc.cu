@@ -93,13 +93,18 @@ __host__ __device__ __forceinline__ int cta_of_tile(int64_t t, int64_t T, int gr
   return static_cast<int>(fdiv64((t + 1) * grid - 1, T));
 }
 
-// every wait of the sketch kernel: try_wait with the plan's suspend-time hint (0 = plain spin)
+// every other wait of the sketch kernel: try_wait with a 10 ms suspend-time hint (development builds:
+// the hint / nanosleep back-off / plain spin is chosen by KRP_TC_WAIT_NS)
+#ifdef KRP_DEV_TRACE
 #define KWAIT(bar, par)                                              \
   do {                                                               \
     if (p.wait_ns >= 100000) mbar_wait_hint((bar), (par), p.wait_ns); \
     else if (p.wait_ns) mbar_wait_sleep((bar), (par), p.wait_ns);    \
     else mbar_wait_spin((bar), (par));                               \
   } while (0)
+#else
+#define KWAIT(bar, par) mbar_wait_hint((bar), (par), 10000000u)
+#endif
 
 // Development timeline (CTA 0 role timestamps): compiled in only with -DKRP_DEV_TRACE, so the
 // production kernel carries no per-chunk trace checks.
@@ -850,9 +855,10 @@ struct RedParams {
 // (32 | 128) nor a region.  A group with a single mode IS that mode's sketch, so its region is written
 // straight into Y (outP / outQ / outT non-null).
 constexpr int kRedWarps = 8;
+constexpr int kAsmMaxOther = 1024;
 __global__ void __launch_bounds__(256) tc_assemble_kernel(const __grid_constant__ RedParams p) {
   __shared__ float red[kRedWarps][32];
-  pdl_wait();  // the partials are written by the sketch kernel
+  __shared__ int s_pnk[kAsmMaxOther];  // slots used by each pair this block reads (computed, not loaded)
   const int w = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
   const int64_t nP = p.do_p ? p.M * p.R : 0, nQ = p.do_q ? p.C * p.R : 0, nT = p.do_t ? p.S * p.R : 0;
   const int64_t bP = p.do_p ? (p.M + 31) / 32 * p.R : 0, bQ = p.do_q ? (p.C + 31) / 32 * p.R : 0;
@@ -881,6 +887,16 @@ __global__ void __launch_bounds__(256) tc_assemble_kernel(const __grid_constant_
     const float* part = (rows ? p.partA1 : p.partA2) + static_cast<int64_t>(r) * kTile + l;
     const int64_t kstride = static_cast<int64_t>(kTile) * p.R;
     const int nother = rows ? p.CB : p.RB;
+    // the slot counts of this block's pairs follow from the static tile split (pure arithmetic), so they
+    // are formed before the wait on the sketch kernel instead of being loaded after it
+    const bool spnk = nother <= kAsmMaxOther;
+    if (spnk)
+      for (int o = static_cast<int>(threadIdx.x); o < nother; o += blockDim.x) {
+        const int64_t pr = rows ? (static_cast<int64_t>(blk) * p.CB + o) : (static_cast<int64_t>(o) * p.CB + blk);
+        s_pnk[o] = cta_of_tile((pr + 1) * p.S - 1, p.T, p.grid) - cta_of_tile(pr * p.S, p.T, p.grid) + 1;
+      }
+    __syncthreads();
+    pdl_wait();  // the partials are written by the sketch kernel
     const int64_t F = static_cast<int64_t>(nother) * p.maxseg;  // flattened (other block, slot) terms
     const int64_t f0 = w * F / kRedWarps, f1 = (w + 1) * F / kRedWarps;
     for (int64_t f = f0; f < f1; f += 8) {
@@ -893,13 +909,15 @@ __global__ void __launch_bounds__(256) tc_assemble_kernel(const __grid_constant_
           const uint32_t f32 = static_cast<uint32_t>(ff), o = f32 / static_cast<uint32_t>(p.maxseg);
           const uint32_t k = f32 - o * static_cast<uint32_t>(p.maxseg);
           const int64_t pair = rows ? (static_cast<int64_t>(blk) * p.CB + o) : (static_cast<int64_t>(o) * p.CB + blk);
-          if (static_cast<int>(k) < __ldg(p.pnk + pair)) v[i] = __ldg(part + (pair * p.maxseg + k) * kstride);
+          const int nk = spnk ? s_pnk[o] : __ldg(p.pnk + pair);
+          if (static_cast<int>(k) < nk) v[i] = __ldg(part + (pair * p.maxseg + k) * kstride);
         }
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i) acc += v[i];
     }
   } else {
+    pdl_wait();  // Tpart is written by the sketch kernel
     const uint32_t idc = static_cast<uint32_t>(idx < nT ? idx : nT - 1);
     const uint32_t s = idc / static_cast<uint32_t>(p.R);
     const int r = static_cast<int>(idc - s * static_cast<uint32_t>(p.R));
