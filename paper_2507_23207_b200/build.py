@@ -16,6 +16,7 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-li
          "-Xptxas", "-v"]
 if os.environ.get("KRP_DEV_TRACE"):  # development: compile the sketch kernel's role timeline in
     FLAGS.append("-DKRP_DEV_TRACE")
+FLAGS += [f"-D{d}" for d in os.environ.get("KRP_NVCC_DEFS", "").split()]  # development A/B builds
 
 
 def _newest_input() -> float:

@@ -129,6 +129,19 @@ __host__ __device__ __forceinline__ int cta_of_tile(int64_t t, int64_t T, int gr
 #define KRP_MMA_SPIN true
 #define KRP_SPLIT_SPIN true
 #endif
+// hot-barrier polling: 0 = spin on try_wait; > 0 = nanosleep back-off of that many ns between probes
+// (a sleeping warp leaves its SMSP's issue slots to the split / epilogue warps sharing it)
+#ifndef KRP_MMA_SLEEP_NS
+#define KRP_MMA_SLEEP_NS 0
+#endif
+#ifndef KRP_SPLIT_SLEEP_NS
+#define KRP_SPLIT_SLEEP_NS 0
+#endif
+#define HOT_WAIT(bar, par, ns)                                  \
+  do {                                                          \
+    if ((ns) > 0) mbar_wait_sleep((bar), (par), (ns) > 0 ? (ns) : 1); \
+    else mbar_wait_spin((bar), (par));                          \
+  } while (0)
 
 __device__ __forceinline__ uint32_t tf32_hi_bits(float x) { return __float_as_uint(x) & 0xFFFFE000u; }
 
@@ -391,14 +404,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         bph ^= 1;
         first = false;
       }
-      if (KRP_MMA_SPIN) mbar_wait_spin(&acc_empty[ast], aph ^ 1); else KWAIT(&acc_empty[ast], aph ^ 1);
+      if (KRP_MMA_SPIN) HOT_WAIT(&acc_empty[ast], aph ^ 1, KRP_MMA_SLEEP_NS); else KWAIT(&acc_empty[ast], aph ^ 1);
       if (leader) KRP_TRACE(3, t - t0);
       tc_fence_after();
       const uint32_t dP = tbase + p.tm_acc + ast * 2 * p.DN;
       const uint32_t dQ = dP + p.DN;
         const uint64_t adesc_t = adesc0 + ((static_cast<uint64_t>(xst) * (kStageFloats * 4)) >> 4);
       for (int kc = 0; kc < nkc; ++kc) {
-        if (KRP_MMA_SPIN) mbar_wait_spin(&chunk_full[cst], cph); else KWAIT(&chunk_full[cst], cph);
+        if (KRP_MMA_SPIN) HOT_WAIT(&chunk_full[cst], cph, KRP_MMA_SLEEP_NS); else KWAIT(&chunk_full[cst], cph);
         if (leader) KRP_TRACE(10, (t - t0) * 8 + kc);
         tc_fence_after();
         const uint32_t ach = tbase + p.tm_chunk + cst * 3 * CH;  // [P hi | P lo | Q lo]
@@ -491,7 +504,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t stage_off = static_cast<uint32_t>(xst) * (kStageFloats * 4u);
       for (int kc = par; kc < nkc; kc += 2) {
         if (sub == 0 && lane == 0) KRP_TRACE(13, (t - t0) * 8 + kc);
-        if (KRP_SPLIT_SPIN) mbar_wait_spin(&chunk_ready[cst], cph ^ 1); else KWAIT(&chunk_ready[cst], cph ^ 1);
+        if (KRP_SPLIT_SPIN) HOT_WAIT(&chunk_ready[cst], cph ^ 1, KRP_SPLIT_SLEEP_NS); else KWAIT(&chunk_ready[cst], cph ^ 1);
         if (sub == 0 && lane == 0) KRP_TRACE(8, (t - t0) * 8 + kc);
         tc_fence_after();
         const uint32_t ch = tbase + lane_off + p.tm_chunk + cst * 3 * CH;
