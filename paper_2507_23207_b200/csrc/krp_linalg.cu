@@ -10,6 +10,7 @@
 //   * squared-difference reduction for ||X - X̂||_F.
 // All cross-block sums are fixed-order (deterministic); no atomics.
 #include <cmath>
+#include <cstdlib>
 
 #include "krp_common.cuh"
 #include "krp_internal.h"
@@ -296,231 +297,123 @@ __global__ void __launch_bounds__(256) ttm_kernel(const float* __restrict__ X, i
   }
 }
 
-// Mode-0 TTM (L == 1, I % 4 == 0, 16-byte aligned X, J <= 40): Y[j + J*h] = sum_i A[j*sj + i*si] X[i + I*h],
-// i.e. the GEMM Y = A X with X column-major (each column h is I contiguous floats).  Block = 256 columns
-// h x all J rows; i in steps of 32 loaded as float4 (8 lanes cover one 128-byte column segment) and
-// transposed into Xs[i][h] (row stride 257: conflict-free stores and loads); warp ty owns rows
-// j = ty*NB + b (b < NB), lane tx owns columns tx + 32k (k < 8).  The output tile is staged through
-// shared memory so that the contiguous range Y[J*h0, J*(h0+256)) is written coalesced.
-constexpr int kM0Cols = 256, kM0K = 32, kM0XS = kM0Cols + 1;
+// Mode-0 TTM, 4 x NB register tiles (L == 1, I % 4 == 0, 16-byte aligned X, J <= 64).  Block = 256
+// columns h x all J rows, 8 warps: warp w owns the row group g = w & 3 (rows g*NB + b, b < NB =
+// ceil(J/4)) and the column half hw = w >> 2; lane l owns the 4 adjacent columns hw*128 + 4l + {0..3}.
+// Per i a thread does one LDS.128 of X and ceil(NB/4) warp-uniform vector loads of A for 4*NB FMAs:
+// FMA-bound, with registers for two blocks per SM.  i advances in steps of 16 (four lanes read one
+// column's 64 contiguous bytes), stored transposed into Xs[i][h ^ 8*((i/4)%4)] (XOR swizzle: conflict-
+// free transposing stores, contiguous float4 reads); the next step is prefetched into registers.  The
+// output tile is staged as Ys[j][h] and written as the contiguous range Y[J*h0, J*(h0+256)).
+constexpr int kQCols = 256, kQK = 16, kQXP = kQCols, kQYP = kQCols + 4;
 template <int NB>
-__global__ void __launch_bounds__(256, 2) ttm_mode0_kernel(const float* __restrict__ X, int64_t I, int64_t H,
-                                                           const float* __restrict__ A, int J, int64_t sj,
-                                                           int64_t si, float* __restrict__ Y) {
-  extern __shared__ float m0s[];
-  float* Xs = m0s;                        // [kM0K][kM0XS]
-  float* As = m0s + kM0K * kM0XS;         // [kM0K][64]: row ii, slot ty*8 + b
-  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
-  const int64_t h0 = static_cast<int64_t>(blockIdx.x) * kM0Cols;
-  // X tile loads: float4 f = tid + 256 k -> i quarter q = f % 8, column hh = f / 8
-  const float4* xptr[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int f = tid + 256 * k;
-    const int64_t h = h0 + (f >> 3);
-    xptr[k] = h < H ? reinterpret_cast<const float4*>(X + h * I) + (f & 7) : nullptr;
-  }
-  float4 xr[8];
-  float ar[8];
-  auto fetch = [&](int64_t i0) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const bool in = xptr[k] && i0 + 4 * ((tid + 256 * k) & 7) < I;
-      xr[k] = in ? __ldg(xptr[k] + (i0 >> 2)) : make_float4(0.f, 0.f, 0.f, 0.f);
-      const int e = tid + 256 * k;  // A slot: (ty', b) = e % 64 -> j = ty' * NB + b, ii = e / 64
-      const int ii = e >> 6, slot = e & 63, tyy = slot >> 3, b = slot & 7;
-      const int j = tyy * NB + b;
-      const int64_t i = i0 + ii;
-      ar[k] = (b < NB && j < J && i < I) ? __ldg(A + j * sj + i * si) : 0.f;
-    }
-  };
-  float acc[8][NB];
-#pragma unroll
-  for (int k = 0; k < 8; ++k)
-#pragma unroll
-    for (int b = 0; b < NB; ++b) acc[k][b] = 0.f;
-  fetch(0);
-  for (int64_t i0 = 0; i0 < I; i0 += kM0K) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int f = tid + 256 * k, q = f & 7, hh = f >> 3;
-      Xs[(4 * q + 0) * kM0XS + hh] = xr[k].x;
-      Xs[(4 * q + 1) * kM0XS + hh] = xr[k].y;
-      Xs[(4 * q + 2) * kM0XS + hh] = xr[k].z;
-      Xs[(4 * q + 3) * kM0XS + hh] = xr[k].w;
-      const int e = tid + 256 * k;
-      As[e] = ar[k];
-    }
-    __syncthreads();
-    if (i0 + kM0K < I) fetch(i0 + kM0K);
-#pragma unroll 4
-    for (int ii = 0; ii < kM0K; ++ii) {
-      const float4 a0 = *reinterpret_cast<const float4*>(As + ii * 64 + ty * 8);
-      const float4 a1 = *reinterpret_cast<const float4*>(As + ii * 64 + ty * 8 + 4);
-      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const float xv = Xs[ii * kM0XS + tx + 32 * k];
-#pragma unroll
-        for (int b = 0; b < NB; ++b) acc[k][b] = fmaf(xv, av[b], acc[k][b]);
-      }
-    }
-    __syncthreads();
-  }
-  // stage the 256 x J output tile (row stride J + 1) and write it out contiguously
-  float* Ys = m0s;
-  const int JS = J + 1;
-#pragma unroll
-  for (int k = 0; k < 8; ++k)
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const int j = ty * NB + b;
-      if (j < J) Ys[(tx + 32 * k) * JS + j] = acc[k][b];
-    }
-  __syncthreads();
-  const int64_t ncols = min(static_cast<int64_t>(kM0Cols), H - h0);
-  const int total = static_cast<int>(ncols) * J;
-  float* out = Y + h0 * J;
-  for (int e = tid; e < total; e += 256) out[e] = Ys[(e / J) * JS + e % J];
-}
-
-size_t ttm_mode0_smem(int J) {
-  const size_t tiles = (static_cast<size_t>(kM0K) * kM0XS + kM0K * 64) * sizeof(float);
-  const size_t out = static_cast<size_t>(kM0Cols) * (J + 1) * sizeof(float);
-  return tiles > out ? tiles : out;
-}
-
-template <int NB>
-int launch_ttm_mode0(const float* X, int64_t I, int64_t H, const float* A, int J, int64_t sj, int64_t si, float* Y,
-                     cudaStream_t s) {
-  const size_t smem = ttm_mode0_smem(J);
-  static size_t set_bytes = 0;
-  if (smem > set_bytes) {
-    KRP_CHECK_CUDA(cudaFuncSetAttribute(ttm_mode0_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(ttm_mode0_smem(64))));
-    set_bytes = ttm_mode0_smem(64);
-  }
-  const unsigned nb = static_cast<unsigned>((H + kM0Cols - 1) / kM0Cols);
-  ttm_mode0_kernel<NB><<<nb, 256, smem, s>>>(X, I, H, A, J, sj, si, Y);
-  KRP_CHECK_LAUNCH();
-  return KRP_OK;
-}
-
-constexpr int kWCols = 512, kWK = 16, kWXP = kWCols, kWYP = kWCols + 4;
-template <int NB4>
-__global__ void __launch_bounds__(256, 1) ttm_mode0w_kernel(const float* __restrict__ X, int64_t I,
-                                                                           int64_t H, const float* __restrict__ A,
-                                                                           int J, int64_t sj, int64_t si,
-                                                                           float* __restrict__ Y) {
-  extern __shared__ __align__(16) float m0w[];
-  float* Xs = m0w;                 // [kWK][kWXP]
-  float* As = m0w + kWK * kWXP;  // [kWK][64]: row ii, slot jg*32 + b
+__global__ void __launch_bounds__(256, 2) ttm_mode0q_kernel(const float* __restrict__ X, int64_t I, int64_t H,
+                                                            const float* __restrict__ A, int J, int64_t sj,
+                                                            int64_t si, float* __restrict__ Y) {
+  extern __shared__ __align__(16) float m0q[];
+  float* Xs = m0q;                // [kQK][kQXP]
+  float* As = m0q + kQK * kQXP;   // [kQK][64]: row ii, slot g*16 + b
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int jg = warp & 1, hg = warp >> 1;
-  const int NB = (J + 1) >> 1;
-  const int64_t h0 = static_cast<int64_t>(blockIdx.x) * kWCols;
-  // X loads: float4 f = tid + 256 k (k < 8): i quarter q = f & 3, column hl = f >> 2 = (tid >> 2) + 64 k, so
-  // 4 lanes read one column's 64 contiguous bytes (coalesced); stored transposed with the column index
-  // XOR-swizzled by 8 q (conflict-free stores, and float4 reads stay contiguous)
+  const int g = warp & 3, hw = warp >> 2;
+  const int64_t h0 = static_cast<int64_t>(blockIdx.x) * kQCols;
   const int lq = tid & 3;
   const int64_t hbase = h0 + (tid >> 2);
   const float* xcol0 = X + hbase * I + 4 * lq;
   const int64_t col64 = 64 * I;
   const int64_t nv64 = H > hbase ? (H - hbase + 63) / 64 : 0;
-  const int nvalid = nv64 < 8 ? static_cast<int>(nv64) : 8;
-  float4 xr[8];
+  const int nvalid = nv64 < 4 ? static_cast<int>(nv64) : 4;
+  float4 xr[4];
   float ar[4];
   auto fetch = [&](int64_t i0) {
     const float* xp = xcol0 + i0;
     const bool iin = i0 + 4 * lq < I;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < 4; ++k) {
       xr[k] = (iin && k < nvalid) ? __ldg(reinterpret_cast<const float4*>(xp)) : make_float4(0.f, 0.f, 0.f, 0.f);
       xp += col64;
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {  // A slot e = tid + 256 k: ii = e >> 6, (jg', b) = e & 63
-      const int e = tid + 256 * k, ii = e >> 6, slot = e & 63, g = slot >> 5, b = slot & 31;
-      const int j = g * NB + b;
+    for (int k = 0; k < 4; ++k) {  // A slot e = tid + 256 k: ii = e >> 6, (g', b) = e & 63
+      const int e = tid + 256 * k, ii = e >> 6, slot = e & 63, gg = slot >> 4, b = slot & 15;
+      const int j = gg * NB + b;
       const int64_t i = i0 + ii;
       ar[k] = (b < NB && j < J && i < I) ? __ldg(A + j * sj + i * si) : 0.f;
     }
   };
-  float acc[4][NB4];
+  float acc[4][NB];
 #pragma unroll
   for (int c = 0; c < 4; ++c)
 #pragma unroll
-    for (int b = 0; b < NB4; ++b) acc[c][b] = 0.f;
+    for (int b = 0; b < NB; ++b) acc[c][b] = 0.f;
   fetch(0);
-  const int xcol = hg * 128 + 4 * lane;
-  const float* as_row = As + jg * 32;
-  for (int64_t i0 = 0; i0 < I; i0 += kWK) {
+  const int xcol = hw * 128 + 4 * lane;
+  const float* as_row = As + g * 16;
+  for (int64_t i0 = 0; i0 < I; i0 += kQK) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < 4; ++k) {
       const int hl = ((tid >> 2) + 64 * k) ^ (8 * lq);
-      Xs[(4 * lq + 0) * kWXP + hl] = xr[k].x;
-      Xs[(4 * lq + 1) * kWXP + hl] = xr[k].y;
-      Xs[(4 * lq + 2) * kWXP + hl] = xr[k].z;
-      Xs[(4 * lq + 3) * kWXP + hl] = xr[k].w;
+      Xs[(4 * lq + 0) * kQXP + hl] = xr[k].x;
+      Xs[(4 * lq + 1) * kQXP + hl] = xr[k].y;
+      Xs[(4 * lq + 2) * kQXP + hl] = xr[k].z;
+      Xs[(4 * lq + 3) * kQXP + hl] = xr[k].w;
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) As[tid + 256 * k] = ar[k];
     __syncthreads();
-    if (i0 + kWK < I) fetch(i0 + kWK);
+    if (i0 + kQK < I) fetch(i0 + kQK);
 #pragma unroll 2
-    for (int ii = 0; ii < kWK; ++ii) {
-      const float4 xv = *reinterpret_cast<const float4*>(Xs + ii * kWXP + (xcol ^ (8 * ((ii >> 2) & 3))));
+    for (int ii = 0; ii < kQK; ++ii) {
+      const float4 xv = *reinterpret_cast<const float4*>(Xs + ii * kQXP + (xcol ^ (8 * ((ii >> 2) & 3))));
+      float av[(NB + 3) / 4 * 4];
 #pragma unroll
-      for (int b4 = 0; b4 < NB4; b4 += 4) {
-        const float4 av = *reinterpret_cast<const float4*>(as_row + ii * 64 + b4);
-        const float a4[4] = {av.x, av.y, av.z, av.w};
+      for (int b4 = 0; b4 < (NB + 3) / 4; ++b4) {
+        const float4 a = *reinterpret_cast<const float4*>(as_row + ii * 64 + 4 * b4);
+        av[4 * b4] = a.x, av[4 * b4 + 1] = a.y, av[4 * b4 + 2] = a.z, av[4 * b4 + 3] = a.w;
+      }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          acc[0][b4 + u] = fmaf(xv.x, a4[u], acc[0][b4 + u]);
-          acc[1][b4 + u] = fmaf(xv.y, a4[u], acc[1][b4 + u]);
-          acc[2][b4 + u] = fmaf(xv.z, a4[u], acc[2][b4 + u]);
-          acc[3][b4 + u] = fmaf(xv.w, a4[u], acc[3][b4 + u]);
-        }
+      for (int b = 0; b < NB; ++b) {
+        acc[0][b] = fmaf(xv.x, av[b], acc[0][b]);
+        acc[1][b] = fmaf(xv.y, av[b], acc[1][b]);
+        acc[2][b] = fmaf(xv.z, av[b], acc[2][b]);
+        acc[3][b] = fmaf(xv.w, av[b], acc[3][b]);
       }
     }
     __syncthreads();
   }
-  // stage Ys[j][h] (float4 over the thread's 4 columns) and write the contiguous output range
-  float* Ys = m0w;
+  float* Ys = m0q;
 #pragma unroll
-  for (int b = 0; b < NB4; ++b) {
-    const int j = jg * NB + b;
-    if (b < NB && j < J)
-      *reinterpret_cast<float4*>(Ys + j * kWYP + hg * 128 + 4 * lane) =
-          make_float4(acc[0][b], acc[1][b], acc[2][b], acc[3][b]);
+  for (int b = 0; b < NB; ++b) {
+    const int j = g * NB + b;
+    if (j < J)
+      *reinterpret_cast<float4*>(Ys + j * kQYP + xcol) = make_float4(acc[0][b], acc[1][b], acc[2][b], acc[3][b]);
   }
   __syncthreads();
-  const int64_t ncols = min(static_cast<int64_t>(kWCols), H - h0);
+  const int64_t ncols = min(static_cast<int64_t>(kQCols), H - h0);
   const int total = static_cast<int>(ncols) * J;
   float* out = Y + h0 * J;
   for (int e = tid; e < total; e += 256) {
     const int h = e / J, j = e - h * J;
-    out[e] = Ys[j * kWYP + h];
+    out[e] = Ys[j * kQYP + h];
   }
 }
 
-size_t ttm_mode0w_smem(int J) {
-  const size_t tiles = (static_cast<size_t>(kWK) * kWXP + kWK * 64) * sizeof(float);
-  const size_t out = static_cast<size_t>(J) * kWYP * sizeof(float);
+size_t ttm_mode0q_smem(int J) {
+  const size_t tiles = (static_cast<size_t>(kQK) * kQXP + kQK * 64) * sizeof(float);
+  const size_t out = static_cast<size_t>(J) * kQYP * sizeof(float);
   return tiles > out ? tiles : out;
 }
 
-template <int NB4>
-int launch_ttm_mode0w(const float* X, int64_t I, int64_t H, const float* A, int J, int64_t sj, int64_t si, float* Y,
-                     cudaStream_t s) {
+template <int NB>
+int launch_ttm_mode0q(const float* X, int64_t I, int64_t H, const float* A, int J, int64_t sj, int64_t si, float* Y,
+                      cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    KRP_CHECK_CUDA(cudaFuncSetAttribute(ttm_mode0w_kernel<NB4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(ttm_mode0w_smem(64))));
+    KRP_CHECK_CUDA(cudaFuncSetAttribute(ttm_mode0q_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(ttm_mode0q_smem(64))));
     attr = true;
   }
-  const unsigned nb = static_cast<unsigned>((H + kWCols - 1) / kWCols);
-  ttm_mode0w_kernel<NB4><<<nb, 256, ttm_mode0w_smem(J), s>>>(X, I, H, A, J, sj, si, Y);
+  const unsigned nb = static_cast<unsigned>((H + kQCols - 1) / kQCols);
+  ttm_mode0q_kernel<NB><<<nb, 256, ttm_mode0q_smem(J), s>>>(X, I, H, A, J, sj, si, Y);
   KRP_CHECK_LAUNCH();
   return KRP_OK;
 }
@@ -893,16 +786,24 @@ int ttm(const float* X, const Dims& g, int n, const float* A, int J, int64_t sj,
   const int64_t L = g.stride[n], I = g.n[n], H = g.N / (L * I);
   const int64_t P = L * H;
   if (P == 0 || J == 0) return KRP_OK;
-  if (L == 1 && J <= 64 && I % 4 == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 && H >= 148 * kM0Cols / 8) {
-    switch ((J + 7) / 8) {
-      case 1: return launch_ttm_mode0<1>(X, I, H, A, J, sj, si, Y, s);
-      case 2: return launch_ttm_mode0<2>(X, I, H, A, J, sj, si, Y, s);
-      case 3: return launch_ttm_mode0<3>(X, I, H, A, J, sj, si, Y, s);
-      case 4: return launch_ttm_mode0<4>(X, I, H, A, J, sj, si, Y, s);
-      case 5: return launch_ttm_mode0<5>(X, I, H, A, J, sj, si, Y, s);
-      case 6: return launch_ttm_mode0w<24>(X, I, H, A, J, sj, si, Y, s);
-      case 7: return launch_ttm_mode0w<28>(X, I, H, A, J, sj, si, Y, s);
-      default: return launch_ttm_mode0w<32>(X, I, H, A, J, sj, si, Y, s);
+  if (L == 1 && J <= 64 && I % 4 == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 && H >= 148 * kQCols / 8) {
+    switch ((J + 3) / 4) {
+      case 1: return launch_ttm_mode0q<1>(X, I, H, A, J, sj, si, Y, s);
+      case 2: return launch_ttm_mode0q<2>(X, I, H, A, J, sj, si, Y, s);
+      case 3: return launch_ttm_mode0q<3>(X, I, H, A, J, sj, si, Y, s);
+      case 4: return launch_ttm_mode0q<4>(X, I, H, A, J, sj, si, Y, s);
+      case 5: return launch_ttm_mode0q<5>(X, I, H, A, J, sj, si, Y, s);
+      case 6: return launch_ttm_mode0q<6>(X, I, H, A, J, sj, si, Y, s);
+      case 7: return launch_ttm_mode0q<7>(X, I, H, A, J, sj, si, Y, s);
+      case 8: return launch_ttm_mode0q<8>(X, I, H, A, J, sj, si, Y, s);
+      case 9: return launch_ttm_mode0q<9>(X, I, H, A, J, sj, si, Y, s);
+      case 10: return launch_ttm_mode0q<10>(X, I, H, A, J, sj, si, Y, s);
+      case 11: return launch_ttm_mode0q<11>(X, I, H, A, J, sj, si, Y, s);
+      case 12: return launch_ttm_mode0q<12>(X, I, H, A, J, sj, si, Y, s);
+      case 13: return launch_ttm_mode0q<13>(X, I, H, A, J, sj, si, Y, s);
+      case 14: return launch_ttm_mode0q<14>(X, I, H, A, J, sj, si, Y, s);
+      case 15: return launch_ttm_mode0q<15>(X, I, H, A, J, sj, si, Y, s);
+      default: return launch_ttm_mode0q<16>(X, I, H, A, J, sj, si, Y, s);
     }
   }
   const unsigned nb = static_cast<unsigned>((P + 63) / 64);
