@@ -131,8 +131,11 @@ __host__ __device__ __forceinline__ int cta_of_tile(int64_t t, int64_t T, int gr
 #endif
 // hot-barrier polling: 0 = spin on try_wait; > 0 = nanosleep back-off of that many ns between probes
 // (a sleeping warp leaves its SMSP's issue slots to the split / epilogue warps sharing it)
+// Measured (profiles/r01j_ab_mma_backoff.log): a 32 ns back-off of the MMA warp's polls helps the wide
+// register-accumulator plans (R8 >= 32: c2 -1.5 %, c3 -1.2 %) and hurts the narrow ones (c4 +3 %), so by
+// default it is applied per instantiation (RA >= 32).
 #ifndef KRP_MMA_SLEEP_NS
-#define KRP_MMA_SLEEP_NS 0
+#define KRP_MMA_SLEEP_NS (RA >= 32 ? 32 : 0)
 #endif
 #ifndef KRP_SPLIT_SLEEP_NS
 #define KRP_SPLIT_SLEEP_NS 0

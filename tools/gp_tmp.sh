@@ -1,5 +1,3 @@
-T=gpurun_out/tq1
+T=gpurun_out/sl3
 mkdir -p $T
-for c in c2 c4 c5; do for v in 1 2 1 2; do echo "variant $v"; KRP_TTM0_VARIANT=$v timeout 120 python tools/rh_time.py $c 5; done; done > $T/log 2>&1
-for v in 1 2; do KRP_TTM0_VARIANT=$v timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:ttm_mode0 -c 2 --csv --log-file $T/ttm_c2_$v.csv python tools/rh_time.py c2 1 > /dev/null 2>&1; done
-timeout 1200 python -m pytest tests -m gpu -x -q -k "rhosvd or sthosvd or tucker or dist" > $T/pytest.log 2>&1
+for c in c2 c3 c4; do for lib in abtest/libkrp_head.so abtest/libkrp_E.so abtest/libkrp_A16.so abtest/libkrp_A32.so abtest/libkrp_A64.so abtest/libkrp_head.so abtest/libkrp_E.so abtest/libkrp_A16.so abtest/libkrp_A32.so abtest/libkrp_A64.so; do echo "lib $lib"; KRP_LIB=$lib timeout 120 python tools/tc_time.py $c 30; done; done > $T/time.log 2>&1
