@@ -134,6 +134,13 @@ __host__ __device__ __forceinline__ int cta_of_tile(int64_t t, int64_t T, int gr
 // Measured (profiles/r01j_ab_mma_backoff.log): a 32 ns back-off of the MMA warp's polls helps the wide
 // register-accumulator plans (R8 >= 32: c2 -1.5 %, c3 -1.2 %) and hurts the narrow ones (c4 +3 %), so by
 // default it is applied per instantiation (RA >= 32).
+// Split-warp roles (profiles/r01j_ab_split_roles.log): with roles, the two warps of a lane quarter share
+// every chunk (P hi / P lo vs Q lo); without, each takes alternate chunks.  Both warps issue from the
+// same SMSP, so roles only pay where the TMEM-accumulator plan leaves the split latency exposed
+// (RA == 0: c5 -3 %); elsewhere alternate chunks are faster (c4 +3..13 % with roles).  -1 = per plan.
+#ifndef KRP_SPLIT_ROLES
+#define KRP_SPLIT_ROLES -1
+#endif
 #ifndef KRP_MMA_SLEEP_NS
 #define KRP_MMA_SLEEP_NS (RA >= 32 ? 32 : 0)
 #endif
@@ -287,6 +294,7 @@ __device__ __forceinline__ void epi_round8(int rnd, float (&acc)[8], uint32_t tD
 template <int CH, int RA>
 __global__ void __launch_bounds__(kThreads, 1)
     krp_tc_sketch_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ TcParams p) {
+  constexpr bool kSplitRoles = KRP_SPLIT_ROLES < 0 ? (RA == 0) : (KRP_SPLIT_ROLES != 0);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* xs = reinterpret_cast<float*>(smem + p.sm_x);
@@ -313,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&empty_x[i], kNumSplitWarps + 1);  // all split warps + the MMA warp's commit
     }
     for (int i = 0; i < p.NC; ++i) {
-      mbar_init(&chunk_full[i], 4);  // the four split warps of this slot
+      mbar_init(&chunk_full[i], kSplitRoles ? kNumSplitWarps : 4);  // split warps writing this slot
       mbar_init(&chunk_ready[i], 1);
     }
     for (int i = 0; i < p.NA; ++i) {
@@ -477,11 +485,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     // P view (lane = ρ): shared-memory loads (the transpose), hi = raw value, lo = x - tf32(x).
     // Q view (lane = γ): 16-byte loads of the rows; only lo goes to TMEM (Q's hi is read from SMEM).
     const uint32_t sub = warp & 3;
-    const int par = static_cast<int>(warp >> 2);  // chunk slot of this warp (NC == 2, nkc even)
+    // kSplitRoles: the two warps of a lane quarter share every chunk, warp w < 4 writing P hi / P lo and
+    // warp w >= 4 Q lo (halves the split latency of a chunk); else warp w takes the chunks kc % 2 == w / 4.
+    const int par = static_cast<int>(warp >> 2);
     const uint32_t lane_off = (32u * sub) << 16;
     int xst = 0;
     uint32_t xph = 0;
-    const bool dop = p.do_p != 0, doq = p.do_q != 0;
+    const bool dop = p.do_p != 0 && (!kSplitRoles || par == 0), doq = p.do_q != 0 && (!kSplitRoles || par == 1);
     // P view: element (ρ = 32*sub + lane, γ) of box `sub` sits at byte γ*128 + (((lane>>2) ^ (γ&7)) << 4) +
     // (lane&3)*4; γ&7 is the compile-time j&7 below, so every load is register + immediate.
     uint32_t psw[8];
@@ -500,12 +510,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         cph ^= 1;
       }
     };
-    if (par) advance();
+    if (!kSplitRoles && par) advance();
+    constexpr int kcStep = kSplitRoles ? 1 : 2;
     for (int64_t t = t0; t < t1; ++t) {
       KWAIT(&full_x[xst], xph);
       if (sub == 0 && lane == 0) KRP_TRACE(1, t - t0);
       const uint32_t stage_off = static_cast<uint32_t>(xst) * (kStageFloats * 4u);
-      for (int kc = par; kc < nkc; kc += 2) {
+      for (int kc = kSplitRoles ? 0 : par; kc < nkc; kc += kcStep) {
         if (sub == 0 && lane == 0) KRP_TRACE(13, (t - t0) * 8 + kc);
         if (KRP_SPLIT_SPIN) HOT_WAIT(&chunk_ready[cst], cph ^ 1, KRP_SPLIT_SLEEP_NS); else KWAIT(&chunk_ready[cst], cph ^ 1);
         if (sub == 0 && lane == 0) KRP_TRACE(8, (t - t0) * 8 + kc);
@@ -557,8 +568,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (sub == 0 && lane == 0) KRP_TRACE(12, (t - t0) * 8 + kc);
         if (lane == 0) mbar_arrive(&chunk_full[cst]);
-        advance();  // skip the other parity's chunk
         advance();
+        if (!kSplitRoles) advance();  // skip the other parity's chunk
       }
       __syncwarp();
       if (sub == 0 && lane == 0) KRP_TRACE(2, t - t0);
