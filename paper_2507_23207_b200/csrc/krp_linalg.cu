@@ -214,17 +214,18 @@ int gram(const T* Y, int64_t rows, int R, double* G, double* partial, cudaStream
 // Generic layout: 64 (l,h) columns x 64 j per block, i in steps of 16.  Each thread's global offsets are
 // fixed across the i loop, so the (l, h) decomposition is done once; the next i step is prefetched into
 // registers while the current one is multiplied.
+template <int JB>  // j per thread (j tile = 16 JB)
 __global__ void __launch_bounds__(256) ttm_kernel(const float* __restrict__ X, int64_t L, int64_t I, int64_t H,
                                                   const float* __restrict__ A, int J, int64_t sj, int64_t si,
                                                   float* __restrict__ Y, int j0) {
   __shared__ float Xs[16][64 + 4];
-  __shared__ float As[16][64 + 4];
+  __shared__ float As[16][16 * JB + 4];
   const int64_t P = L * H;
   const int64_t p0 = static_cast<int64_t>(blockIdx.x) * 64;
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  int xi[4], xp[4], ai[4], aj[4];
+  int xi[4], xp[4], ai[JB], aj[JB];
   int64_t xoff[4];
-  const float* aptr[4];
+  const float* aptr[JB];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int e = threadIdx.x + 256 * k;
@@ -241,46 +242,52 @@ __global__ void __launch_bounds__(256) ttm_kernel(const float* __restrict__ X, i
       const int64_t l = p % L, h = p / L;
       xoff[k] = l + L * I * h;
     }
+  }
+#pragma unroll
+  for (int k = 0; k < JB; ++k) {
+    const int e = threadIdx.x + 256 * k;
     ai[k] = e % 16;
     aj[k] = e / 16;
     const int j = j0 + aj[k];
     aptr[k] = j < J ? A + j * sj : nullptr;
   }
-  float xr[4], ar[4];
+  float xr[4], ar[JB];
   auto fetch = [&](int64_t i0) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int64_t i = i0 + xi[k];
       xr[k] = (xoff[k] >= 0 && i < I) ? __ldg(X + xoff[k] + L * i) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < JB; ++k) {
       const int64_t ia = i0 + ai[k];
       ar[k] = (aptr[k] && ia < I) ? __ldg(aptr[k] + ia * si) : 0.f;
     }
   };
-  float acc[4][4];
+  float acc[4][JB];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
+    for (int b = 0; b < JB; ++b) acc[a][b] = 0.f;
   fetch(0);
   for (int64_t i0 = 0; i0 < I; i0 += 16) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      Xs[xi[k]][xp[k]] = xr[k];
-      As[ai[k]][aj[k]] = ar[k];
-    }
+    for (int k = 0; k < 4; ++k) Xs[xi[k]][xp[k]] = xr[k];
+#pragma unroll
+    for (int k = 0; k < JB; ++k) As[ai[k]][aj[k]] = ar[k];
     __syncthreads();
     if (i0 + 16 < I) fetch(i0 + 16);
 #pragma unroll
     for (int ii = 0; ii < 16; ++ii) {
-      float xv[4], av[4];
+      float xv[4], av[JB];
 #pragma unroll
       for (int a = 0; a < 4; ++a) xv[a] = Xs[ii][tx + 16 * a];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) av[b] = As[ii][ty + 16 * b];
+      for (int b = 0; b < JB; ++b) av[b] = As[ii][ty + 16 * b];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(xv[a], av[b], acc[a][b]);
+        for (int b = 0; b < JB; ++b) acc[a][b] = fmaf(xv[a], av[b], acc[a][b]);
     }
     __syncthreads();
   }
@@ -290,7 +297,7 @@ __global__ void __launch_bounds__(256) ttm_kernel(const float* __restrict__ X, i
     if (p >= P) continue;
     const int64_t l = p % L, h = p / L;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
+    for (int b = 0; b < JB; ++b) {
       const int j = j0 + ty + 16 * b;
       if (j < J) Y[l + L * (j + static_cast<int64_t>(J) * h)] = acc[a][b];
     }
@@ -807,8 +814,14 @@ int ttm(const float* X, const Dims& g, int n, const float* A, int J, int64_t sj,
     }
   }
   const unsigned nb = static_cast<unsigned>((P + 63) / 64);
-  for (int j0 = 0; j0 < J; j0 += 64) {
-    ttm_kernel<<<nb, 256, 0, s>>>(X, L, I, H, A, J, sj, si, Y, j0);
+  const int jb = J >= 64 ? 4 : (J + 15) / 16;  // j tile 16 jb: no more than 15 padded j per launch
+  for (int j0 = 0; j0 < J; j0 += 16 * jb) {
+    switch (jb) {
+      case 1: ttm_kernel<1><<<nb, 256, 0, s>>>(X, L, I, H, A, J, sj, si, Y, j0); break;
+      case 2: ttm_kernel<2><<<nb, 256, 0, s>>>(X, L, I, H, A, J, sj, si, Y, j0); break;
+      case 3: ttm_kernel<3><<<nb, 256, 0, s>>>(X, L, I, H, A, J, sj, si, Y, j0); break;
+      default: ttm_kernel<4><<<nb, 256, 0, s>>>(X, L, I, H, A, J, sj, si, Y, j0); break;
+    }
     KRP_CHECK_LAUNCH();
   }
   return KRP_OK;
