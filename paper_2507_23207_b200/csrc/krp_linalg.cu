@@ -398,9 +398,17 @@ __global__ void __launch_bounds__(256, 2) ttm_mode0q_kernel(const float* __restr
   const int64_t ncols = min(static_cast<int64_t>(kQCols), H - h0);
   const int total = static_cast<int>(ncols) * J;
   float* out = Y + h0 * J;
+  // e = h * J + j advanced by 256 per step without a division per element
+  int h = tid / J, j = tid - (tid / J) * J;
+  const int dh = 256 / J, dj = 256 - dh * J;
   for (int e = tid; e < total; e += 256) {
-    const int h = e / J, j = e - h * J;
     out[e] = Ys[j * kQYP + h];
+    h += dh;
+    j += dj;
+    if (j >= J) {
+      j -= J;
+      ++h;
+    }
   }
 }
 
