@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(256) ttm_kernel(const float* __restrict__ X, i
 // output tile is staged as Ys[j][h] and written as the contiguous range Y[J*h0, J*(h0+256)).
 constexpr int kQCols = 256, kQK = 16, kQXP = kQCols, kQYP = kQCols + 4;
 template <int NB>
-__global__ void __launch_bounds__(256, 2) ttm_mode0q_kernel(const float* __restrict__ X, int64_t I, int64_t H,
+__global__ void __launch_bounds__(256, NB <= 5 ? 3 : 2) ttm_mode0q_kernel(const float* __restrict__ X, int64_t I, int64_t H,
                                                             const float* __restrict__ A, int J, int64_t sj,
                                                             int64_t si, float* __restrict__ Y) {
   extern __shared__ __align__(16) float m0q[];
