@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(256) chol_inv_kernel(const double* __restrict_
   double(*Li)[kGramMaxR + 1] = reinterpret_cast<double(*)[kGramMaxR + 1]>(dyn_smem + kGramMaxR * (kGramMaxR + 1));
   __shared__ int fail;
   __shared__ double shift;
+  __shared__ double rdiag[kGramMaxR];  // 1 / L[j][j]
   const int tid = threadIdx.x, nt = blockDim.x;  // 256 threads: a 16 x 16 grid for the rank-1 updates
   const int tx = tid & 15, ty = tid >> 4;
   if (tid == 0) shift = 0.0;
@@ -106,10 +107,13 @@ __global__ void __launch_bounds__(256) chol_inv_kernel(const double* __restrict_
         if (tid == 0) fail = 1;
         break;
       }
-      const double ljj = sqrt(dgl);
+      const double rl = rsqrt(dgl);  // 1 / L[j][j]: one reciprocal square root instead of sqrt + divides
       __syncthreads();  // all threads have read A[j][j]
-      for (int i = j + 1 + tid; i < R; i += nt) A[i][j] /= ljj;
-      if (tid == 0) A[j][j] = ljj;
+      for (int i = j + 1 + tid; i < R; i += nt) A[i][j] *= rl;
+      if (tid == 0) {
+        A[j][j] = dgl * rl;  // L[j][j] = sqrt(dgl)
+        rdiag[j] = rl;
+      }
       __syncthreads();
       // trailing (i, k), j < k <= i < R, on a 16 x 16 thread grid (no integer division)
       for (int i = j + 1 + ty; i < R; i += 16) {
@@ -141,8 +145,8 @@ __global__ void __launch_bounds__(256) chol_inv_kernel(const double* __restrict_
   for (int e = tid; e < R * R; e += nt) Li[e / R][e % R] = (e / R == e % R) ? 1.0 : 0.0;
   __syncthreads();
   for (int i = 0; i < R; ++i) {
-    const double d = A[i][i];
-    for (int c = tid; c <= i; c += nt) Li[i][c] /= d;
+    const double rd = rdiag[i];
+    for (int c = tid; c <= i; c += nt) Li[i][c] *= rd;
     __syncthreads();
     for (int r = i + 1 + ty; r < R; r += 16) {  // rows i+1..R-1, columns 0..i
       const double lri = A[r][i];
