@@ -1,10 +1,5 @@
-T=gpurun_out/ch2
+T=gpurun_out/df1
 mkdir -p $T
-{
-for c in c2 c3 c2 c3; do
-  echo "== head"; KRP_LIB=abtest/libkrp_head.so timeout 120 python tools/rh_time.py $c 10
-  echo "== new";  timeout 120 python tools/rh_time.py $c 10
-done
-} > $T/log 2>&1
-timeout 1500 python -m pytest tests -m gpu -x -q > $T/pytest.log 2>&1
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:chol -c 3 --csv --log-file $T/chol.csv python tools/rh_time.py c2 1 > /dev/null 2>&1
+for c in c4 c2; do for o in 0 9 0 9; do echo "opt $o"; KRP_LIB=abtest/libkrp_df.so KRP_TC_OPT=$o timeout 60 python tools/tc_time.py $c 30 check | grep -v "mode [1-9]"; done; done > $T/time.log 2>&1
+echo "current lib" >> $T/time.log
+for c in c4 c2; do timeout 60 python tools/tc_time.py $c 30; done >> $T/time.log 2>&1
