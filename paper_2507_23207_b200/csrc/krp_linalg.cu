@@ -243,7 +243,15 @@ __global__ void __launch_bounds__(256) ttm_kernel(const float* __restrict__ X, i
     const int64_t p = p0 + xp[k];
     xoff[k] = -1;
     if (p < P) {
-      const int64_t l = p % L, h = p / L;
+      int64_t l, h;
+      if (P < (int64_t(1) << 31)) {  // 32-bit division where the column index fits (the common case)
+        const uint32_t p32 = static_cast<uint32_t>(p), L32 = static_cast<uint32_t>(L);
+        h = p32 / L32;
+        l = p32 - static_cast<uint32_t>(h) * L32;
+      } else {
+        l = p % L;
+        h = p / L;
+      }
       xoff[k] = l + L * I * h;
     }
   }
@@ -299,7 +307,15 @@ __global__ void __launch_bounds__(256) ttm_kernel(const float* __restrict__ X, i
   for (int a = 0; a < 4; ++a) {
     const int64_t p = p0 + tx + 16 * a;
     if (p >= P) continue;
-    const int64_t l = p % L, h = p / L;
+    int64_t l, h;
+    if (P < (int64_t(1) << 31)) {
+      const uint32_t p32 = static_cast<uint32_t>(p), L32 = static_cast<uint32_t>(L);
+      h = p32 / L32;
+      l = p32 - static_cast<uint32_t>(h) * L32;
+    } else {
+      l = p % L;
+      h = p / L;
+    }
 #pragma unroll
     for (int b = 0; b < JB; ++b) {
       const int j = j0 + ty + 16 * b;

@@ -1,5 +1,9 @@
-T=gpurun_out/df1
+T=gpurun_out/tg4
 mkdir -p $T
-for c in c4 c2; do for o in 0 9 0 9; do echo "opt $o"; KRP_LIB=abtest/libkrp_df.so KRP_TC_OPT=$o timeout 60 python tools/tc_time.py $c 30 check | grep -v "mode [1-9]"; done; done > $T/time.log 2>&1
-echo "current lib" >> $T/time.log
-for c in c4 c2; do timeout 60 python tools/tc_time.py $c 30; done >> $T/time.log 2>&1
+{
+for c in c4 c3 c2 c4 c3 c2; do
+  echo "== head"; KRP_LIB=abtest/libkrp_head.so timeout 120 python tools/rh_time.py $c 5
+  echo "== new";  timeout 120 python tools/rh_time.py $c 5
+done
+} > $T/log 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q > $T/pytest.log 2>&1
