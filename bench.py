@@ -9,7 +9,7 @@ One timed step of the headline = one krp_sketch_all_modes call (memoized all-mod
 (rows a1-a9: sketch, CholeskyQR, core, truncation) -> "rhosvd_s".
 value = 4*N*R*K / t  (algorithmic TFLOP/s), t = max over ranks of CUDA-event time.
 
-  python bench.py [--gpus N --steps K --warmup W] [--config c2] [--engine auto|tc|simt]
+  python bench.py [--gpus N --steps K --warmup W] [--config c5]
   python bench.py --impl reference ...   # the fp64 oracle on host cores (bounded sample per step)
 """
 from __future__ import annotations
@@ -198,7 +198,6 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    krp.krp_set_engine({"auto": 0, "tc": 1, "simt": 2}[args.engine])
     Id = cfg.dims[-1]
     k0, kn = krp.krp_slab_range(Id, world, rank)  # the library's slab geometry
     k1 = k0 + kn
@@ -288,7 +287,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     if os.path.exists(tpath):
         with open(tpath) as f:
             tj = json.load(f)
-        ent = tj.get(f"{cfg.name}:{args.engine}:{world}") or tj.get(f"{cfg.name}:{args.engine}")
+        ent = tj.get(f"{cfg.name}:{world}") or tj.get(cfg.name)
         if ent:
             traffic = ent.get("dram_bytes_per_launch")
     if bound == "hbm":
@@ -373,7 +372,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded Tucker/smooth tensors of BASELINE.json's configs; no dataset)",
-            "config": _workload(cfg, world), "engine": args.engine,
+            "config": _workload(cfg, world),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "rhosvd_s": rhosvd_s, "rhosvd_rel_err": rel_err,
             "pct_roofline": 100.0 * max(t_hbm, t_tc) / (t_ms / 1e3 / args.steps),
@@ -389,7 +388,6 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="c2", choices=sorted(synth.CONFIGS))
-    ap.add_argument("--engine", default="auto", choices=["auto", "tc", "simt"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-rhosvd", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

@@ -52,13 +52,14 @@ extern "C" {
 
 typedef enum krp_status {
   KRP_OK = 0,
-  KRP_EINVAL = 1,       /* null pointer, d not in [2,8], R not in [1,128], dim < 1, n out of range */
+  KRP_EINVAL = 1,       /* null pointer, d not in [2,8], R not in [1,256] (rhosvd/sthosvd: [1,64]), dim < 1,
+                           n out of range */
   KRP_ESHAPE = 2,       /* r_n > R, R > min(I_n, N/I_n), inconsistent slab geometry */
   KRP_ECUDA = 3,        /* a CUDA runtime / launch error */
   KRP_ENCCL = 4,        /* NCCL unavailable or a collective failed */
   KRP_ENUMERIC = 5,     /* CholeskyQR failed even after the shifted fallback */
   KRP_ENOMEM = 6,       /* ws_bytes < krp_workspace_bytes(...) or allocation failed */
-  KRP_EUNSUPPORTED = 7  /* no kernel for this device (requires sm_100a) */
+  KRP_EUNSUPPORTED = 7  /* the device is not sm_100a (B200): the library has no other code path */
 } krp_status;
 
 /* op codes for krp_workspace_bytes */
@@ -71,17 +72,9 @@ enum {
   KRP_OP_RHOSVD_ERR = 5       /* krp_rhosvd with rel_err != NULL */
 };
 
-/* Sketch engine selection (krp_set_engine); default KRP_ENGINE_AUTO. */
-enum {
-  KRP_ENGINE_AUTO = 0, /* tcgen05 3xTF32 kernel where the shape is supported, else SIMT */
-  KRP_ENGINE_TC = 1,   /* force the tcgen05 kernel (KRP_EUNSUPPORTED if the shape is not supported) */
-  KRP_ENGINE_SIMT = 2  /* force the fp32 CUDA-core kernel */
-};
-
 KRP_API const char* krp_status_string(int status);
 KRP_API const char* krp_last_error_message(void);
 KRP_API int krp_version(void);
-KRP_API int krp_set_engine(int engine);
 
 /* Workspace size in bytes for `op` (one of KRP_OP_*).  ranks may be NULL for the sketch ops. */
 KRP_API size_t krp_workspace_bytes(int op, int d, const int64_t* dims, int R, const int* ranks);

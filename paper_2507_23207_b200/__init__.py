@@ -20,7 +20,7 @@ import torch
 __all__ = [
     "krp_profile_enable", "krp_profile_read", "krp_profile_reset",
     "lib", "KrpError", "OP_SKETCH_ALL", "OP_SKETCH_MODE", "OP_RHOSVD", "OP_STHOSVD", "OP_SKETCH_ALL_HOST",
-    "OP_RHOSVD_ERR", "ENGINE_AUTO", "ENGINE_TC", "ENGINE_SIMT", "krp_set_engine", "krp_workspace_bytes",
+    "OP_RHOSVD_ERR", "krp_workspace_bytes",
     "krp_sketch_all_modes", "krp_sketch_all_modes_host", "krp_sketch_mode", "krp_rhosvd", "krp_sthosvd",
     "krp_launch_count", "krp_reset_launch_count", "Comm", "krp_sketch_all_modes_dist", "krp_rhosvd_dist",
     "krp_workspace_bytes_dist", "EXPORTED_SYMBOLS", "LIB_PATH", "krp_slab_range", "krp_pack_layout",
@@ -28,11 +28,10 @@ __all__ = [
 
 LIB_PATH = os.environ.get("KRP_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libkrp.so")
 OP_SKETCH_ALL, OP_SKETCH_MODE, OP_RHOSVD, OP_STHOSVD, OP_SKETCH_ALL_HOST, OP_RHOSVD_ERR = range(6)
-ENGINE_AUTO, ENGINE_TC, ENGINE_SIMT = range(3)
 
 # every function declared in include/krp.h
 EXPORTED_SYMBOLS = [
-    "krp_status_string", "krp_last_error_message", "krp_version", "krp_set_engine", "krp_workspace_bytes",
+    "krp_status_string", "krp_last_error_message", "krp_version", "krp_workspace_bytes",
     "krp_sketch_all_modes", "krp_sketch_all_modes_host", "krp_sketch_mode", "krp_rhosvd", "krp_sthosvd",
     "krp_comm_id_bytes", "krp_comm_get_unique_id", "krp_comm_init", "krp_comm_destroy",
     "krp_sketch_all_modes_dist", "krp_rhosvd_dist", "krp_workspace_bytes_dist", "krp_launch_count",
@@ -67,7 +66,6 @@ def lib() -> ctypes.CDLL:
         l_.krp_status_string.argtypes = [ctypes.c_int]
         l_.krp_last_error_message.restype = ctypes.c_char_p
         l_.krp_version.restype = ctypes.c_int
-        l_.krp_set_engine.argtypes = [ctypes.c_int]
         l_.krp_workspace_bytes.restype = ctypes.c_size_t
         l_.krp_workspace_bytes.argtypes = [ctypes.c_int, ctypes.c_int, _I64P, ctypes.c_int, _IP]
         l_.krp_workspace_bytes_dist.restype = ctypes.c_size_t
@@ -134,10 +132,6 @@ def _ws(nbytes: int, device, ws: Optional[torch.Tensor]):
             raise ValueError("workspace tensor too small")
         return ws
     return torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
-
-
-def krp_set_engine(engine: int) -> None:
-    _check(lib().krp_set_engine(int(engine)), "krp_set_engine")
 
 
 def krp_workspace_bytes(op: int, dims: Sequence[int], R: int, ranks: Optional[Sequence[int]] = None) -> int:

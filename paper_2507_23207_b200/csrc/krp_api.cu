@@ -16,7 +16,7 @@
 
 namespace krp {
 
-// ------------------------------------------------------------------ errors / counters / engine
+// ------------------------------------------------------------------ errors / counters
 static thread_local char g_err[512] = "";
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -28,8 +28,6 @@ const char* last_error() { return g_err; }
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n)); }
-
-static std::atomic<int> g_engine{KRP_ENGINE_AUTO};
 
 // ---- kernel profiling
 struct ProfRec {
@@ -99,8 +97,8 @@ static int validate_ranks(const Dims& g, const int* ranks, int R) {
     set_error("ranks is NULL");
     return KRP_EINVAL;
   }
-  if (R > 64) {
-    set_error("rhosvd/sthosvd support R <= 64 (got %d)", R);
+  if (R > kMaxRDecomp) {  // reading R20: the decompositions take R <= 64
+    set_error("rhosvd/sthosvd support R <= %d (got %d)", kMaxRDecomp, R);
     return KRP_EINVAL;
   }
   for (int k = 0; k < g.d; ++k) {
@@ -113,31 +111,6 @@ static int validate_ranks(const Dims& g, const int* ranks, int R) {
       return KRP_ESHAPE;
     }
   }
-  return KRP_OK;
-}
-
-// ------------------------------------------------------------------ sketch dispatch
-size_t sketch_ws_bytes(const Dims& g, int R, const bool* want) {
-  size_t b = 0;
-  const int eng = g_engine.load();
-  if (eng != KRP_ENGINE_SIMT && tc_sketch_supported(g, R, want)) b = std::max(b, tc_sketch_ws_bytes(g, R, want));
-  for (int k = 0; k < g.d; ++k)
-    if (want[k]) b = std::max(b, simt_sketch_ws_bytes(g, k, R));
-  return b;
-}
-
-int sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const bool* want, float* const* Y, Arena& ar,
-           cudaStream_t s) {
-  const int eng = g_engine.load();
-  if (eng != KRP_ENGINE_SIMT) {
-    if (tc_sketch_supported(g, R, want)) return tc_sketch(X, g, om, R, want, Y, ar, s);
-    if (eng == KRP_ENGINE_TC) {
-      set_error("tcgen05 engine does not support this shape/device");
-      return KRP_EUNSUPPORTED;
-    }
-  }
-  for (int k = 0; k < g.d; ++k)
-    if (want[k]) KRP_TRY(simt_sketch_mode(X, g, k, om, R, Y[k], ar, s));
   return KRP_OK;
 }
 
@@ -231,14 +204,16 @@ static int ttm_chain(const float* X, Dims g, const TtmOp* ops, float* bufA, floa
 struct DistCtx;
 // Per-device side streams for independent per-mode work (the d CholeskyQR2 factorisations of rHOSVD):
 // forked from and joined back into the caller's stream with events, so the caller sees one ordered
-// stream (and a captured graph gets parallel branches).
+// stream (and a captured graph gets parallel branches).  The fork / join events are shared, so a caller
+// holds the per-device lock from the fork record until its stream has waited on every join event
+// (concurrent rhosvd calls from several host threads on one device serialise only that enqueue section).
 struct SideStreams {
   cudaStream_t st[kMaxD];
   cudaEvent_t fork, join[kMaxD];
   bool ok = false;
 };
-static std::mutex g_side_mu;
-static int side_streams(SideStreams** out) {
+static std::mutex g_side_mu[64];
+static int side_streams(SideStreams** out, std::unique_lock<std::mutex>& lk) {
   static SideStreams per_dev[64];
   int dev = 0;
   KRP_CHECK_CUDA(cudaGetDevice(&dev));
@@ -246,7 +221,7 @@ static int side_streams(SideStreams** out) {
     set_error("device ordinal %d out of range", dev);
     return KRP_EINVAL;
   }
-  std::lock_guard<std::mutex> lk(g_side_mu);
+  lk = std::unique_lock<std::mutex>(g_side_mu[dev]);
   SideStreams& ss = per_dev[dev];
   if (!ss.ok) {
     for (int k = 0; k < kMaxD; ++k) {
@@ -452,7 +427,8 @@ static int rhosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_t
   //      side streams (each is a chain of small latency-bound kernels)
   {
     SideStreams* ss = nullptr;
-    KRP_TRY(side_streams(&ss));
+    std::unique_lock<std::mutex> side_lock;  // held until s has waited on every join event
+    KRP_TRY(side_streams(&ss, side_lock));
     KRP_CHECK_CUDA(cudaEventRecord(ss->fork, s));
     size_t off = scratch_mark;
     for (int k = 0; k < d; ++k) {
@@ -714,14 +690,6 @@ const char* krp_status_string(int st) {
 
 const char* krp_last_error_message(void) { return krp::last_error(); }
 int krp_version(void) { return 10000; }
-int krp_set_engine(int engine) {
-  if (engine < KRP_ENGINE_AUTO || engine > KRP_ENGINE_SIMT) {
-    krp::set_error("bad engine %d", engine);
-    return KRP_EINVAL;
-  }
-  krp::g_engine.store(engine);
-  return KRP_OK;
-}
 uint64_t krp_launch_count(void) { return krp::g_launches.load(); }
 
 int krp_profile_enable(int on) {
@@ -1012,6 +980,10 @@ int krp_slab_range(int64_t I_d, int nranks, int rank, int64_t* begin, int64_t* l
   if (I_d < 1 || nranks < 1 || rank < 0 || rank >= nranks || !begin || !len) {
     set_error("krp_slab_range: bad arguments");
     return KRP_EINVAL;
+  }
+  if (nranks > I_d) {  // every rank must own a non-empty slab (all ranks take this branch together)
+    set_error("krp_slab_range: %d ranks > I_d = %lld (empty slabs)", nranks, static_cast<long long>(I_d));
+    return KRP_ESHAPE;
   }
   const int64_t b = I_d * rank / nranks, e = I_d * (rank + 1) / nranks;
   *begin = b;

@@ -11,7 +11,8 @@
 namespace krp {
 
 constexpr int kMaxD = 8;
-constexpr int kMaxR = 128;
+constexpr int kMaxR = 256;      // sketch width R; rhosvd / sthosvd: R <= kMaxRDecomp
+constexpr int kMaxRDecomp = 64; // the fp64 Gram / Cholesky / Jacobi kernels hold R x R in one CTA
 
 // Tensor geometry, first-index-fastest.
 struct Dims {

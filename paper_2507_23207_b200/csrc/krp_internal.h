@@ -4,22 +4,18 @@
 
 namespace krp {
 
-// ---- sketch engines
-size_t simt_sketch_ws_bytes(const Dims& g, int n, int R);
-int simt_sketch_mode(const float* X, const Dims& g, int n, const OmegaPtrs& om, int R, float* Y, Arena& ar,
-                     cudaStream_t s);
-
-// tcgen05 3xTF32 engine.  want_mode[k] selects which Y_k are produced.  Returns
-// KRP_EUNSUPPORTED (without launching) when the shape/device is not supported.
-bool tc_sketch_supported(const Dims& g, int R, const bool* want_mode);
+// ---- the sketch (krp_sketch_tc.cu): tcgen05 3xTF32 kernels for every shape; want_mode[k] selects which
+// Y_k are produced.  R in [1, 256] (column groups of <= 64 per launch).  KRP_EUNSUPPORTED (nothing
+// launched) on a device that is not sm_100a.
+bool tc_device_ok();
 size_t tc_sketch_ws_bytes(const Dims& g, int R, const bool* want_mode);
 int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const bool* want_mode, float* const* Y,
               Arena& ar, cudaStream_t s);
-
-// Dispatch over engines (krp_set_engine); Y[k] for every k with want_mode[k].
-size_t sketch_ws_bytes(const Dims& g, int R, const bool* want_mode);
-int sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const bool* want_mode, float* const* Y,
-           Arena& ar, cudaStream_t s);
+inline size_t sketch_ws_bytes(const Dims& g, int R, const bool* want_mode) { return tc_sketch_ws_bytes(g, R, want_mode); }
+inline int sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const bool* want_mode, float* const* Y,
+                  Arena& ar, cudaStream_t s) {
+  return tc_sketch(X, g, om, R, want_mode, Y, ar, s);
+}
 
 // ---- dense linear algebra (krp_linalg.cu)
 // CholeskyQR with shifted first pass and two refinement passes (sCholeskyQR3; plain CholeskyQR2

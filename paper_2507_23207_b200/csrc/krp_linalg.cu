@@ -175,15 +175,13 @@ struct EigBatch;
 __global__ void jacobi_top_kernel(EigBatch batch, int J);
 constexpr size_t kSquareSmem = 2 * kGramMaxR * (kGramMaxR + 1) * sizeof(double);
 constexpr size_t kJacobiSmem = 3 * kGramMaxR * (kGramMaxR + 1) * sizeof(double);
+// The raised shared-memory limits are a per-device function attribute: set on every call (cheap host call),
+// so a second device in the process and concurrent host threads see them too.
 int set_square_smem_attrs() {
-  static int done = 0;
-  if (!done) {
-    KRP_CHECK_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(kSquareSmem)));
-    KRP_CHECK_CUDA(cudaFuncSetAttribute(jacobi_top_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(kJacobiSmem)));
-    done = 1;
-  }
+  KRP_CHECK_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kSquareSmem)));
+  KRP_CHECK_CUDA(cudaFuncSetAttribute(jacobi_top_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kJacobiSmem)));
   return KRP_OK;
 }
 
@@ -441,12 +439,8 @@ size_t ttm_mode0q_smem(int J) {
 template <int NB>
 int launch_ttm_mode0q(const float* X, int64_t I, int64_t H, const float* A, int J, int64_t sj, int64_t si, float* Y,
                       cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    KRP_CHECK_CUDA(cudaFuncSetAttribute(ttm_mode0q_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(ttm_mode0q_smem(64))));
-    attr = true;
-  }
+  KRP_CHECK_CUDA(cudaFuncSetAttribute(ttm_mode0q_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(ttm_mode0q_smem(64))));  // per device: set every call
   const unsigned nb = static_cast<unsigned>((H + kQCols - 1) / kQCols);
   ttm_mode0q_kernel<NB><<<nb, 256, ttm_mode0q_smem(J), s>>>(X, I, H, A, J, sj, si, Y);
   KRP_CHECK_LAUNCH();

@@ -797,7 +797,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ------------------------------------------------------------------ Khatri-Rao tables
 struct TabParams {
-  int d, m, m2, R, RS, R8, NP, RB, CB;
+  int d, m, m2, R, RS, R8, NP, RB, CB, ldo;
   int64_t M, C, S;
   int64_t n[kMaxD];
   int64_t gs[kMaxD];
@@ -833,7 +833,7 @@ __global__ void tc_tables_kernel(const __grid_constant__ TabParams p) {
       for (int k = rows ? 0 : p.m; k < (rows ? p.m : p.m2); ++k) {
         if (!p.om[k]) continue;  // Ω_n of a single-mode sketch is not given: it never reaches Y_n
         const uint32_t ik = (lin / static_cast<uint32_t>(p.gs[k])) % static_cast<uint32_t>(p.n[k]);
-        w *= __ldg(p.om[k] + static_cast<size_t>(ik) * p.R + r);
+        w *= __ldg(p.om[k] + static_cast<size_t>(ik) * p.ldo + r);
       }
       const float whi = __uint_as_float(tf32_hi_bits(w));
       v = (n < p.R) ? whi : w - whi;
@@ -852,7 +852,7 @@ __global__ void tc_tables_kernel(const __grid_constant__ TabParams p) {
       for (int k = p.m2; k < p.d; ++k) {
         if (!p.om[k]) continue;
         const uint32_t ik = (sl / static_cast<uint32_t>(p.gs[k])) % static_cast<uint32_t>(p.n[k]);
-        w *= __ldg(p.om[k] + static_cast<size_t>(ik) * p.R + r);
+        w *= __ldg(p.om[k] + static_cast<size_t>(ik) * p.ldo + r);
       }
     }
     p.OmS[idx] = w;
@@ -865,7 +865,7 @@ __global__ void tc_tables_kernel(const __grid_constant__ TabParams p) {
 // ------------------------------------------------------------------ reduction of partials + multi-TTVs
 struct RedParams {
   int64_t M, C, S, T;
-  int RB, CB, R, grid, maxseg;
+  int RB, CB, R, grid, maxseg, ldy;
   int do_p, do_q, do_t;
   const float *partA1, *partA2, *Tpart;
   const int* pnk;  // slots used per pair (slots k >= pnk[pair] are not read)
@@ -902,6 +902,8 @@ __global__ void __launch_bounds__(256) tc_assemble_kernel(const __grid_constant_
   int64_t idx = blk_id * 32 + lane;  // Ts: linear (s, r); P / Qc: replaced by rho * R + r below
   bool valid = true;
   float acc = 0.f;
+  int64_t outi = 0;  // output row (ρ, γ or s) and column, for the strided direct write into Y
+  int outr = 0;
   if (region < 2) {
     const bool rows = region == 0;
     const int64_t nrow = rows ? p.M : p.C;
@@ -910,6 +912,8 @@ __global__ void __launch_bounds__(256) tc_assemble_kernel(const __grid_constant_
     valid = rho < nrow;
     const int64_t rc = valid ? rho : nrow - 1;
     idx = rc * p.R + r;
+    outi = rc;
+    outr = r;
     const int blk = static_cast<int>(rc / kTile), l = static_cast<int>(rc % kTile);
     const float* part = (rows ? p.partA1 : p.partA2) + static_cast<int64_t>(r) * kTile + l;
     const int64_t kstride = static_cast<int64_t>(kTile) * p.R;
@@ -948,6 +952,8 @@ __global__ void __launch_bounds__(256) tc_assemble_kernel(const __grid_constant_
     const uint32_t idc = static_cast<uint32_t>(idx < nT ? idx : nT - 1);
     const uint32_t s = idc / static_cast<uint32_t>(p.R);
     const int r = static_cast<int>(idc - s * static_cast<uint32_t>(p.R));
+    outi = s;
+    outr = r;
     const int64_t npairs = static_cast<int64_t>(p.RB) * p.CB;
     const int64_t p0 = w * npairs / kRedWarps, p1 = (w + 1) * npairs / kRedWarps;
     const int64_t pstride = p.S * p.R;
@@ -967,8 +973,11 @@ __global__ void __launch_bounds__(256) tc_assemble_kernel(const __grid_constant_
 #pragma unroll
     for (int i = 1; i < kRedWarps; ++i) tot += red[i][lane];
     const int64_t n = region == 0 ? nP : (region == 1 ? nQ : nT);
-    float* out = region == 0 ? (p.outP ? p.outP : p.Pm) : (region == 1 ? (p.outQ ? p.outQ : p.Qc) : (p.outT ? p.outT : p.Ts));
-    if (valid && idx < n) out[idx] = tot;
+    float* direct = region == 0 ? p.outP : (region == 1 ? p.outQ : p.outT);
+    if (valid && idx < n) {
+      if (direct) direct[outi * p.ldy + outr] = tot;  // a single-mode group: its Y (row stride ldy)
+      else (region == 0 ? p.Pm : (region == 1 ? p.Qc : p.Ts))[idx] = tot;
+    }
   }
 }
 
@@ -977,7 +986,7 @@ int64_t assemble_blocks(int64_t M, int64_t C, int64_t S, int R, int do_p, int do
 }
 
 struct TtvParams {
-  int d, m, m2, R;
+  int d, m, m2, R, ldo, ldy;
   int64_t M, C, S;
   int64_t n[kMaxD];
   int64_t gs[kMaxD];
@@ -1036,7 +1045,7 @@ __global__ void __launch_bounds__(256) tc_ttv_kernel(const __grid_constant__ Ttv
           const uint32_t nj = static_cast<uint32_t>(p.n[j]), q = rem / nj, ij = rem - q * nj;
           rem = q;
           lin += ij * static_cast<uint32_t>(p.gs[j]);
-          wt *= __ldg(p.om[j] + static_cast<size_t>(ij) * p.R + r);
+          wt *= __ldg(p.om[j] + static_cast<size_t>(ij) * p.ldo + r);
         }
         xv[u] = __ldg(src + static_cast<size_t>(lin) * p.R + r);
         wv[u] = wt;
@@ -1051,7 +1060,7 @@ __global__ void __launch_bounds__(256) tc_ttv_kernel(const __grid_constant__ Ttv
     double tot = red[0][lane];
 #pragma unroll
     for (int u = 1; u < kRedWarps; ++u) tot += red[u][lane];
-    if (idx < cnt) p.y[k][static_cast<size_t>(i) * p.R + r] = static_cast<float>(tot);
+    if (idx < cnt) p.y[k][static_cast<size_t>(i) * p.ldy + r] = static_cast<float>(tot);
   }
 }
 
@@ -1059,7 +1068,9 @@ __global__ void __launch_bounds__(256) tc_ttv_kernel(const __grid_constant__ Ttv
 struct TcPlan {
   bool ok = false;
   int m = 0, m2 = 0;
-  int64_t M = 0, C = 0, S = 0;
+  int64_t M = 0, Mp = 0, C = 0, S = 0;  // Mp: rows as TMA sees them (M rounded up to 4 when repacked)
+  bool repack = false;                  // X staged into a padded copy (row pitch not a 16-byte multiple, or
+                                        // a base address that is not 16-byte aligned)
   int RB = 0, CB = 0;
   int64_t T = 0;
   int R = 0, NP = 0, N2 = 0, R8 = 0, RS = 0, NS = 0, NC = 0, NA = 0, CH = 16, triple = 0, DN = 0, RA = 0;
@@ -1069,44 +1080,49 @@ struct TcPlan {
   uint32_t sm_x = 0, sm_bp = 0, sm_bq = 0, sm_red = 0, sm_bar = 0, sm_ws = 0, smem_bytes = 0;
 };
 
-int num_sms() {
-  static int n = -1;
-  if (n < 0) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) !=
-                                                   cudaSuccess)
-      n = 148;
-  }
-  return n;
-}
-
-bool device_is_sm100() {
-  static int ok = -1;
-  if (ok < 0) {
-    int dev = 0, major = 0, minor = 0;
-    ok = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess &&
-        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) == cudaSuccess &&
+struct DevInfo {
+  int sms = 148;
+  bool sm100 = false;
+};
+// per device (a process may drive several GPUs), computed once under a once-flag
+const DevInfo& dev_info() {
+  static DevInfo info[64];
+  static std::once_flag once[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  std::call_once(once[dev], [dev] {
+    DevInfo& di = info[dev];
+    int major = 0, minor = 0, n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) di.sms = n;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) == cudaSuccess &&
         cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) == cudaSuccess)
-      ok = (major == 10 && minor == 0) ? 1 : 0;
+      di.sm100 = (major == 10 && minor == 0);
     cudaGetLastError();
-  }
-  return ok == 1;
+  });
+  return info[dev];
 }
+int num_sms() { return dev_info().sms; }
+bool device_is_sm100() { return dev_info().sm100; }
 
 int round16(int v) { return (v + 15) / 16 * 16; }
 
-// Fill geometry for a grouping (m, m2) and check the kernel's constraints.
-bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, TcPlan& pl) {
+// Fill geometry for a grouping (m, m2) and check the kernel's constraints.  Group sizes below 128 are
+// covered by TMA's out-of-bounds zero fill (partial row / column blocks); a row pitch that is not a multiple
+// of 16 bytes (M % 4 != 0) needs the padded copy (allow_repack).
+bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, bool allow_repack, TcPlan& pl) {
   pl = TcPlan{};
   int64_t M = 1, C = 1, S = 1;
   for (int k = 0; k < m; ++k) M *= g.n[k];
   for (int k = m; k < m2; ++k) C *= g.n[k];
   for (int k = m2; k < g.d; ++k) S *= g.n[k];
-  if (M < kTile || C < kTile || (M % 4) != 0) return false;
+  const bool need_repack = (M % 4) != 0;
+  if (need_repack && !allow_repack) return false;
+  const int64_t Mp = (M + 3) / 4 * 4;
   // the table / assembly kernels use 32-bit index math
-  if (M * kMaxTcR >= (int64_t(1) << 31) || C * kMaxTcR >= (int64_t(1) << 31) || S * kMaxTcR >= (int64_t(1) << 31))
+  if (Mp * kMaxTcR >= (int64_t(1) << 31) || C * kMaxTcR >= (int64_t(1) << 31) || S * kMaxTcR >= (int64_t(1) << 31))
     return false;
+  pl.Mp = Mp;
+  pl.repack = need_repack;
   bool wr = false, wc = false, ws = false;
   for (int k = 0; k < g.d; ++k) {
     if (!want[k]) continue;
@@ -1119,7 +1135,7 @@ bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, TcPlan& pl
   pl.M = M;
   pl.C = C;
   pl.S = S;
-  pl.RB = static_cast<int>((M + kTile - 1) / kTile);
+  pl.RB = static_cast<int>((Mp + kTile - 1) / kTile);
   pl.CB = static_cast<int>((C + kTile - 1) / kTile);
   pl.T = static_cast<int64_t>(pl.RB) * pl.CB * S;
   pl.R = R;
@@ -1189,14 +1205,18 @@ bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, TcPlan& pl
   return true;
 }
 
-bool choose_plan(const Dims& g, int R, const bool* want, TcPlan& best) {
+// Groupings that TMA can view directly are preferred; the padded copy (an extra pass over X) is used only
+// when no grouping has a 16-byte row pitch, or always when force_repack (X not 16-byte aligned).
+bool choose_plan(const Dims& g, int R, const bool* want, bool force_repack, TcPlan& best) {
   if (R > kMaxTcR || R < 1) return false;
   bool found = false;
   double best_cost = 1e300;
+  for (int pass = 0; pass < 2 && !found; ++pass)
   for (int m = 1; m < g.d; ++m) {
     for (int m2 = m + 1; m2 <= g.d; ++m2) {
       TcPlan pl;
-      if (!fill_plan(g, R, m, m2, want, pl)) continue;
+      if (!fill_plan(g, R, m, m2, want, pass == 1 || force_repack, pl)) continue;
+      if (force_repack) pl.repack = true;
       // cost in units of one tile-GEMM: MMA work incl. ragged-tile waste, plus the per-segment
       // overhead (B operand generation + partial flush + assembly, ~8 tile-GEMMs per (rb, cb)
       // pair) — a grouping without slice modes (S = 1) makes every tile its own segment.
@@ -1230,7 +1250,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 long long* g_trace_dev = nullptr;
 
 struct WsLayout {
-  size_t a1, a2, slots, pnk, tpart, pm, qc, ts, wl, wr, oms, total;
+  size_t a1, a2, slots, pnk, tpart, pm, qc, ts, wl, wr, oms, xp, total;
 };
 WsLayout ws_layout(const TcPlan& pl) {
   WsLayout w{};
@@ -1252,29 +1272,72 @@ WsLayout ws_layout(const TcPlan& pl) {
   w.wl = take(static_cast<size_t>(pl.RB) * pl.NP * kTile * sizeof(float));  // B_Q images
   w.wr = take(static_cast<size_t>(pl.CB) * pl.NP * kTile * sizeof(float));  // B_P images
   w.oms = take(static_cast<size_t>(pl.S) * pl.RS * sizeof(float));
+  w.xp = take(pl.repack ? static_cast<size_t>(pl.Mp) * pl.C * pl.S * sizeof(float) : 0);
   w.total = off;
   return w;
 }
 
-}  // namespace
-
-bool tc_sketch_supported(const Dims& g, int R, const bool* want) {
-  if (!device_is_sm100() || !get_encode()) return false;
-  TcPlan pl;
-  return choose_plan(g, R, want, pl);
+// Input staging for shapes TMA cannot view: Xp(ρ, rest) = X(ρ, rest) for ρ < M, 0 for M <= ρ < Mp
+// (Mp = round4(M): a 16-byte row pitch); also used when X is not 16-byte aligned.  One extra pass over X.
+__global__ void repack_rows_kernel(const float* __restrict__ X, int64_t M, int64_t Mp, int64_t cols,
+                                   float* __restrict__ Xp) {
+  const int64_t total = Mp * cols;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = e / Mp, r = e - c * Mp;
+    Xp[e] = r < M ? X[c * M + r] : 0.f;
+  }
 }
 
+size_t plan_ws_bytes(const Dims& g, int R, const bool* want) {
+  size_t b = 0;
+  for (int rep = 0; rep < 2; ++rep) {  // with and without the padded copy (alignment is known only at call time)
+    TcPlan pl;
+    if (choose_plan(g, R, want, rep == 1, pl)) b = std::max(b, ws_layout(pl).total);
+  }
+  return b;
+}
+
+int tc_sketch_cols(const float* X, const Dims& g, const OmegaPtrs& om, int R, int ldo, const bool* want,
+                   float* const* Y, int ldy, Arena& ar, cudaStream_t s);
+
+}  // namespace
+
+bool tc_device_ok() { return device_is_sm100() && get_encode() != nullptr; }
+
+// Columns of a KRP sketch are independent (Lemma 2.3): R > 64 runs as column groups of <= 64
+// columns (one pass over X each), Ω and Y addressed through their row stride R.
 size_t tc_sketch_ws_bytes(const Dims& g, int R, const bool* want) {
-  TcPlan pl;
-  if (!choose_plan(g, R, want, pl)) return 0;
-  return ws_layout(pl).total;
+  size_t b = 0;
+  for (int c0 = 0; c0 < R; c0 += kMaxTcR) b = std::max(b, plan_ws_bytes(g, std::min(kMaxTcR, R - c0), want));
+  return b;
 }
 
 int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const bool* want, float* const* Y, Arena& ar,
               cudaStream_t s) {
+  if (!tc_device_ok()) {
+    set_error("the KRP sketch needs an sm_100a device (B200) and the driver's TMA encoder");
+    return KRP_EUNSUPPORTED;
+  }
+  for (int c0 = 0; c0 < R; c0 += kMaxTcR) {
+    OmegaPtrs oc{};
+    float* Yc[kMaxD] = {};
+    for (int k = 0; k < g.d; ++k) {
+      oc.p[k] = om.p[k] ? om.p[k] + c0 : nullptr;
+      Yc[k] = (want[k] && Y[k]) ? Y[k] + c0 : nullptr;
+    }
+    KRP_TRY(tc_sketch_cols(X, g, oc, std::min(kMaxTcR, R - c0), R, want, Yc, R, ar, s));
+  }
+  return KRP_OK;
+}
+
+namespace {
+int tc_sketch_cols(const float* X, const Dims& g, const OmegaPtrs& om, int R, int ldo, const bool* want,
+                   float* const* Y, int ldy, Arena& ar, cudaStream_t s) {
   TcPlan pl;
-  if (!device_is_sm100() || !choose_plan(g, R, want, pl)) {
-    set_error("tcgen05 sketch: unsupported shape/device");
+  const bool misaligned = (reinterpret_cast<uintptr_t>(X) & 15u) != 0;
+  if (!choose_plan(g, R, want, misaligned, pl)) {
+    set_error("tcgen05 sketch: no tiling for this shape");
     return KRP_EUNSUPPORTED;
   }
   auto encode = get_encode();
@@ -1288,6 +1351,15 @@ int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const b
   if (ar.overflow()) {
     set_error("workspace too small for the tcgen05 sketch");
     return KRP_ENOMEM;
+  }
+  const float* Xv = X;
+  if (pl.repack) {  // stage X with a 16-byte row pitch (and a 16-byte aligned base)
+    float* Xp = reinterpret_cast<float*>(wsb + wl.xp);
+    const int64_t total = pl.Mp * pl.C * pl.S;
+    const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, static_cast<int64_t>(num_sms()) * 16));
+    repack_rows_kernel<<<blocks, 256, 0, s>>>(X, pl.M, pl.Mp, pl.C * pl.S, Xp);
+    KRP_CHECK_LAUNCH();
+    Xv = Xp;
   }
   TcParams p{};
   p.M = pl.M;
@@ -1361,12 +1433,12 @@ int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const b
 
   CUtensorMap tmap;
   {
-    cuuint64_t dims[3] = {static_cast<cuuint64_t>(pl.M), static_cast<cuuint64_t>(pl.C),
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(pl.Mp), static_cast<cuuint64_t>(pl.C),
                           static_cast<cuuint64_t>(pl.S)};
-    cuuint64_t strides[2] = {static_cast<cuuint64_t>(pl.M) * 4, static_cast<cuuint64_t>(pl.M * pl.C) * 4};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(pl.Mp) * 4, static_cast<cuuint64_t>(pl.Mp * pl.C) * 4};
     cuuint32_t box[3] = {32, 128, 1};
     cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(X), dims, strides, box, estr,
+    CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(Xv), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
@@ -1386,6 +1458,7 @@ int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const b
     tp.NP = pl.NP;
     tp.RB = pl.RB;
     tp.CB = pl.CB;
+    tp.ldo = ldo;
     tp.M = pl.M;
     tp.C = pl.C;
     tp.S = pl.S;
@@ -1449,6 +1522,7 @@ int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const b
     rp.R = R;
     rp.grid = pl.grid;
     rp.maxseg = pl.maxseg;
+    rp.ldy = ldy;
     rp.do_p = pl.do_p;
     rp.do_q = pl.do_q;
     rp.do_t = pl.do_t;
@@ -1478,6 +1552,8 @@ int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const b
     tv.m = pl.m;
     tv.m2 = pl.m2;
     tv.R = R;
+    tv.ldo = ldo;
+    tv.ldy = ldy;
     tv.M = pl.M;
     tv.C = pl.C;
     tv.S = pl.S;
@@ -1504,4 +1580,5 @@ int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const b
   return KRP_OK;
 }
 
+}  // namespace
 }  // namespace krp

@@ -54,7 +54,11 @@ def test_argument_validation_without_device(krp):
     assert lib.krp_sketch_all_modes(1, 9, dims, ptrs, 4, ptrs, None, 0, None) == 1
     # R out of range
     assert lib.krp_sketch_all_modes(1, 3, dims, ptrs, 0, ptrs, None, 0, None) == 1
-    assert lib.krp_sketch_all_modes(1, 3, dims, ptrs, 129, ptrs, None, 0, None) == 1
+    assert lib.krp_sketch_all_modes(1, 3, dims, ptrs, 257, ptrs, None, 0, None) == 1
+    # rhosvd / sthosvd take R <= 64 (reading R20)
+    r3 = (ctypes.c_int * 3)(2, 2, 2)
+    big = (ctypes.c_int64 * 3)(128, 128, 128)
+    assert lib.krp_rhosvd(1, 3, big, r3, 65, ptrs, ptrs, 1, None, None, 0, None) == 1
     # empty mode (a dimension of size 0) and negative sizes are rejected before any launch
     for bad_dims in ((8, 0, 8), (0, 8, 8), (8, 8, -1)):
         dz = (ctypes.c_int64 * 3)(*bad_dims)

@@ -89,6 +89,10 @@ def test_slab_range_and_pack_layout_host_only():
     build.build()
     for Id in (1, 7, 64, 512):
         for G in (1, 2, 3, 8):
+            if G > Id:  # every rank must own a non-empty slab: all ranks fail together, before any collective
+                with pytest.raises(krp.KrpError):
+                    krp.krp_slab_range(Id, G, 0)
+                continue
             spans = [krp.krp_slab_range(Id, G, g) for g in range(G)]
             assert spans[0][0] == 0 and sum(n for _, n in spans) == Id
             for (b0, n0), (b1, _) in zip(spans, spans[1:]):
