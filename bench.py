@@ -1,8 +1,10 @@
 #!/usr/bin/env python
 """bench.py — all-mode KRP sketch throughput (and rHOSVD time) on B200, BASELINE.json's metric.
 
-Default (N=1): BASELINE configs[1] = c2, a 512^3 fp32 Tucker(30^3, decay 0.8) + 1e-3 noise tensor,
-R = 40, inputs resident in HBM (512 MiB > 126 MB L2, so no L2 flush is needed between steps).
+Default (N=1): BASELINE configs[4] = c5, the largest single-GPU config (2048 x 2048 x 512 fp32 smooth
+tensor + 1e-6 noise, R = 60, 8 GiB resident in HBM: larger than L2, no flush needed), the tensor the
+8-GPU scaling target names.  Inputs under 2x L2 (c1) are flushed between timed steps.  The same line
+carries per-config kernel fractions for c2-c5 ("per_config") and the c3 STHOSVD time.
 
 One timed step of the headline = one krp_sketch_all_modes call (memoized all-mode sketch, SURVEY
 §8(a) rows a1-a6, including the NCCL combine at N>1).  The same run also times K full rHOSVD steps
@@ -191,6 +193,40 @@ def run_reference(args, cfg, rank, world):
 
 
 # ------------------------------------------------------------------ our arm
+def _roofline(cfg_dims, R, k_ms, k_n, k_bytes, k_flops, steps):
+    """Roofline of the dominant sketch kernel: algorithmic bytes (4 B per element, X read once) or flops
+    (4NR) per launch over its CUDA-event duration, against MEASURED_PEAKS.json."""
+    N = float(np.prod(cfg_dims))
+    hbm_gbs, bf16_tf, peak_src = _peaks()
+    p3 = bf16_tf * (1.1 / 2.25) / 3.0  # tf32 = bf16 x nominal 1.1/2.25; 3xTF32 = three tf32 products
+    t_hbm = 4.0 * N / (hbm_gbs * 1e9)
+    t_tc = 4.0 * N * R / (p3 * 1e12)
+    bound = "hbm" if t_hbm >= t_tc else "tensor"
+    avg_s = (k_ms / 1e3) / max(k_n, 1)
+    if bound == "hbm":
+        achieved = (k_bytes / max(k_n, 1)) / avg_s / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_gbs, "unit": "GB/s", "frac": achieved / hbm_gbs}
+    else:
+        achieved = (k_flops / max(k_n, 1)) / avg_s / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": p3, "unit": "TFLOP/s", "frac": achieved / p3}
+    roof.update({"peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs / bf16_tflops burst; "
+                                f"3xTF32 = bf16 x 1.1/2.25 / 3)",
+                 "kernel_ms_avg": 1e3 * avg_s, "kernel_launches_per_step": k_n / max(steps, 1),
+                 "roof_ms": 1e3 * max(t_hbm, t_tc)})
+    return roof
+
+
+def _traffic(name, world):
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            tj = json.load(f)
+        ent = tj.get(f"{name}:{world}") or tj.get(name)
+        if ent:
+            return ent.get("dram_bytes_per_launch")
+    return None
+
+
 def run_ours(args, cfg, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -202,7 +238,6 @@ def run_ours(args, cfg, rank, world, local_rank):
     k0, kn = krp.krp_slab_range(Id, world, rank)  # the library's slab geometry
     k1 = k0 + kn
     dims_local = list(cfg.dims[:-1]) + [k1 - k0]
-    n_local = int(np.prod(dims_local))
     x_host = torch.from_numpy(synth.tensor_slab(cfg, args.seed, k0, k1)).pin_memory()
     om_np = synth.omegas(cfg.dims, cfg.R, args.seed)
     om_host = [torch.from_numpy(o).pin_memory() for o in om_np]
@@ -210,6 +245,10 @@ def run_ours(args, cfg, rank, world, local_rank):
     om = [o.to(dev) for o in om_host]
     comm = krp.Comm() if world > 1 else None
     stream = torch.cuda.current_stream()
+    l2_bytes = int(getattr(torch.cuda.get_device_properties(dev), "L2_cache_size", 126 * 2 ** 20))
+    # inputs smaller than twice the L2 are flushed between timed steps (a write of 2x L2, outside the events)
+    flush = 4 * int(np.prod(dims_local)) < 2 * l2_bytes
+    flush_buf = torch.empty(2 * l2_bytes // 4, dtype=torch.float32, device=dev) if flush else None
 
     if world > 1:
         ws = torch.empty(krp.krp_workspace_bytes_dist(krp.OP_SKETCH_ALL, dims_local, Id, cfg.R), dtype=torch.uint8,
@@ -236,20 +275,45 @@ def run_ours(args, cfg, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    def timed(fn, steps, sampler=None):
+    def timed(fn, steps, sampler=None, flush_l2=False):
+        """Device time of `steps` calls (CUDA events on the launching stream), max over ranks.  With flush_l2
+        every step is bracketed by its own events and preceded (outside them) by a 2x-L2 write."""
         barrier()
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if sampler:
             sampler.start()
-        e0.record(stream)
-        for _ in range(steps):
-            fn()
-        e1.record(stream)
-        torch.cuda.synchronize()
+        if flush_l2:
+            evs = []
+            for _ in range(steps):
+                flush_buf.fill_(1.0)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                fn()
+                e1.record(stream)
+                evs.append((e0, e1))
+            torch.cuda.synchronize()
+            ms = sum(a.elapsed_time(b) for a, b in evs)
+        else:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(steps):
+                fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
         clocks = sampler.stop() if sampler else None
         barrier()
-        return max_over_ranks(e0.elapsed_time(e1)), clocks
+        return max_over_ranks(ms), clocks
+
+    def kernel_profile(fn, steps, flush_l2=False):
+        """The dominant kernel's own event time (library profiler, events on the launching stream)."""
+        krp.krp_profile_reset()
+        krp.krp_profile_enable(True)
+        timed(fn, steps, flush_l2=flush_l2)
+        krp.krp_profile_enable(False)
+        r = krp.krp_profile_read()
+        krp.krp_profile_reset()
+        return r
 
     # ---- phase A: the headline all-mode sketch
     for _ in range(args.warmup):
@@ -258,52 +322,18 @@ def run_ours(args, cfg, rank, world, local_rank):
     krp.krp_reset_launch_count()
     gpu_index = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local_rank)).split(",")[0]) \
         if os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")[0].isdigit() else local_rank
-    t_ms, clocks = timed(sketch, args.steps, ClockSampler(gpu_index) if rank == 0 else None)
+    t_ms, clocks = timed(sketch, args.steps, ClockSampler(gpu_index) if rank == 0 else None, flush_l2=flush)
     launches = krp.krp_launch_count()
-    # the dominant kernel's own duration: a second pass with CUDA events around each of its launches
-    # (on the launching stream); kept out of the headline loop so the events do not perturb it
-    krp.krp_profile_reset()
-    krp.krp_profile_enable(True)
-    timed(sketch, args.steps)
-    krp.krp_profile_enable(False)
-    k_ms, k_n, k_bytes, k_flops = krp.krp_profile_read()
-    krp.krp_profile_reset()
-    k_steps = args.steps
+    # the dominant kernel's own duration: a second pass with CUDA events around each of its launches (on the
+    # launching stream); kept out of the headline loop so the events do not perturb it
+    k_ms, k_n, k_bytes, k_flops = kernel_profile(sketch, args.steps, flush_l2=flush)
     flops_step = 4.0 * cfg.N * cfg.R
     value = flops_step * args.steps / (t_ms / 1e3) / 1e12
+    roof = _roofline(dims_local, cfg.R, k_ms, k_n, k_bytes, k_flops, args.steps)
+    roof["traffic"] = _traffic(cfg.name, world)
+    roof["kernel_share_of_step"] = (k_ms / args.steps) / (t_ms / args.steps)
 
-    # ---- roofline of the dominant kernel (algorithmic bytes / flops per launch over its event time)
-    hbm_gbs, bf16_tf, peak_src = _peaks()
-    tf32_tf = bf16_tf * (1.1 / 2.25)          # guide's nominal dense tf32 : bf16 ratio
-    p3 = tf32_tf / 3.0                        # 3xTF32 split: three tf32 products per fp32 product
-    t_hbm = 4.0 * cfg.N / (hbm_gbs * 1e9)
-    t_tc = flops_step / (p3 * 1e12)
-    bound = "hbm" if t_hbm >= t_tc else "tensor"
-    avg_launch_s = (k_ms / 1e3) / max(k_n, 1)
-    bytes_per_launch = k_bytes / max(k_n, 1)
-    flops_per_launch = k_flops / max(k_n, 1)
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as f:
-            tj = json.load(f)
-        ent = tj.get(f"{cfg.name}:{world}") or tj.get(cfg.name)
-        if ent:
-            traffic = ent.get("dram_bytes_per_launch")
-    if bound == "hbm":
-        achieved = bytes_per_launch / avg_launch_s / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_gbs, "unit": "GB/s", "frac": achieved / hbm_gbs,
-                "traffic": traffic}
-    else:
-        achieved = flops_per_launch / avg_launch_s / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": p3, "unit": "TFLOP/s", "frac": achieved / p3,
-                "traffic": traffic}
-    roof.update({"peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs burst; 3xTF32 = bf16 x 1.1/2.25 / 3)",
-                 "kernel_ms_avg": 1e3 * avg_launch_s, "kernel_launches_per_step": k_n / k_steps,
-                 "kernel_share_of_step": (k_ms / k_steps) / (t_ms / args.steps),
-                 "roof_ms_step": 1e3 * max(t_hbm, t_tc)})
-
-    # ---- phase B: full rHOSVD steps (sketch + QR + core + truncation)
+    # ---- phase B: full rHOSVD steps (sketch + QR + core + truncation) on the headline tensor
     rhosvd_s = None
     rel_err = None
     if not args.no_rhosvd:
@@ -350,14 +380,61 @@ def run_ours(args, cfg, rank, world, local_rank):
                 torch.cuda.current_stream().synchronize()
         for _ in range(min(args.warmup, 2)):
             e2e_step()
-        steps_e = max(1, min(args.steps, 10))
+        steps_e = max(1, min(args.steps, 5))
         te, _ = timed(e2e_step, steps_e)
-        h2d = 4 * (int(np.prod(cfg.dims)) + sum(n * cfg.R for n in cfg.dims))
-        d2h = 4 * sum(n * cfg.R for n in cfg.dims) * world
-        e2e = {"value": flops_step * steps_e / (te / 1e3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": te / steps_e}
+        h2d = 4 * (int(np.prod(dims_local)) + sum(n * cfg.R for n in cfg.dims))
+        d2h = 4 * sum(n * cfg.R for n in cfg.dims)
+        e2e = {"value": flops_step * steps_e / (te / 1e3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d * world,
+               "d2h_bytes_per_step": d2h * world, "ms_per_step": te / steps_e}
         if world == 1:
             del wsh
+
+    # ---- per-config kernel fractions (c2-c5, and STHOSVD time on c3), rank 0 at N = 1: N(0,1) device data of
+    # each config's shape (the sketch's time does not depend on the values), the same kernel profiler
+    per_config = None
+    if rank == 0 and world == 1 and not args.no_per_config:
+        per_config = {}
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(1234)
+        for name in ("c2", "c3", "c4", "c5"):
+            c = synth.config(name)
+            if name == cfg.name:
+                Xc, omc = X, om
+            else:
+                Xc = torch.randn(c.N, generator=gen, device=dev, dtype=torch.float32)
+                omc = [torch.randn((n, c.R), generator=gen, device=dev, dtype=torch.float32) for n in c.dims]
+            Yc = [torch.empty((n, c.R), dtype=torch.float32, device=dev) for n in c.dims]
+            wsc = torch.empty(krp.krp_workspace_bytes(krp.OP_SKETCH_ALL, c.dims, c.R), dtype=torch.uint8, device=dev)
+
+            def sk(Xc=Xc, omc=omc, Yc=Yc, wsc=wsc, c=c):
+                krp.krp_sketch_all_modes(Xc, c.dims, omc, Y=Yc, ws=wsc)
+            for _ in range(3):
+                sk()
+            nst = 10
+            tms, _ = timed(sk, nst)
+            kr = kernel_profile(sk, nst)
+            rf = _roofline(c.dims, c.R, *kr, nst)
+            entry = {"dims": list(c.dims), "R": c.R, "step_ms": tms / nst, "tflops_step": 4.0 * c.N * c.R / (tms / nst / 1e3) / 1e12,
+                     "bound": rf["bound"], "achieved": rf["achieved"], "unit": rf["unit"], "frac": rf["frac"],
+                     "kernel_ms_avg": rf["kernel_ms_avg"], "roof_ms": rf["roof_ms"], "traffic": _traffic(name, 1),
+                     "data": "N(0,1) device data of the config's shape" if name != cfg.name else "the headline tensor"}
+            if name == "c3":  # the c3 workload is STHOSVD (Alg. 8)
+                oms3 = synth.sthosvd_omegas(c.dims, c.R, 0)
+                dom = [[None if o is None else torch.from_numpy(o).to(dev) for o in row] for row in oms3]
+                wss = torch.empty(krp.krp_workspace_bytes(krp.OP_STHOSVD, c.dims, c.R, c.ranks), dtype=torch.uint8,
+                                  device=dev)
+
+                def st(Xc=Xc, dom=dom, wss=wss, c=c):
+                    krp.krp_sthosvd(Xc, c.dims, c.ranks, dom, ws=wss)
+                st()
+                ts_, _ = timed(st, 3)
+                entry["sthosvd_s"] = ts_ / 1e3 / 3
+                del wss
+            per_config[name] = entry
+            del Yc, wsc
+            if name != cfg.name:
+                del Xc, omc
+            torch.cuda.empty_cache()
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
@@ -367,37 +444,56 @@ def run_ours(args, cfg, rank, world, local_rank):
     if comm is not None:
         comm.close()
     if rank == 0:
+        wl = _workload(cfg, world)
+        wl["l2"] = ("inputs smaller than 2x L2: a 2x-L2 write between timed steps, outside the step events"
+                    if flush else "inputs larger than 2x L2 (no flush needed)")
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded Tucker/smooth tensors of BASELINE.json's configs; no dataset)",
-            "config": _workload(cfg, world),
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clocks, "rhosvd_s": rhosvd_s, "rhosvd_rel_err": rel_err,
-            "pct_roofline": 100.0 * max(t_hbm, t_tc) / (t_ms / 1e3 / args.steps),
+            "config": wl, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clocks, "rhosvd_s": rhosvd_s, "rhosvd_rel_err": rel_err, "per_config": per_config,
         }
         print(json.dumps(line), flush=True)
     return 0
 
 
+def _free_port():
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    return port
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="c2", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--config", default="c5", choices=sorted(synth.CONFIGS))
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-rhosvd", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-per-config", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = synth.config(args.config)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # launched without torchrun: start one rank per GPU ourselves (same arguments), rank 0 prints the line
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+        return 2
     if args.impl == "reference":
         return run_reference(args, cfg, rank, world)
     if world > 1:
