@@ -1,11 +1,16 @@
-"""GPU parity at BASELINE.json's FULL sizes, in the launch configuration bench.py times (default engine,
-caller-provided workspace): sampled rows of every Y_n against the fp64 oracle computed row by row
-(oracle.sketch_rows_ttv, the column identity of P:85-93), and the Tucker error of the full decompositions.
+"""GPU parity at BASELINE.json's FULL sizes, in the launch configuration bench.py times (caller-provided
+workspace, the default plan), against the fp64 oracle on the same seeded inputs.
 
-Tolerances (BASELINE north_star): per-mode relative Frobenius error of Y_n <= 1e-5 (here over the
-sampled rows); |e_gpu - e_oracle| <= 1e-4 (reading R12).  c4/c5 are too large for the fp64 oracle's
-full rHOSVD, so there the GPU's reported error is checked against a Monte-Carlo estimate of
-||X - [G; Q]||_F / ||X||_F from 2^18 sampled entries reconstructed on the host from the GPU factors."""
+* Sketch: every element of every Y_n at c2 and c3 (and c4, marked slow) against the oracle's full
+  explicit-Khatri-Rao sketch (chunked over the last mode: same terms, fp64); at c5, two rows in every
+  128-row block of every mode by the column identity (oracle.sketch_rows_ttv).
+* rHOSVD: the reported Tucker error against the oracle's own rHOSVD at c2, c4 and c5 (|Δ| <= 1e-4, reading
+  R12, and <= 1 % relative: at c5 the error is ~1.3e-6, where the absolute bar alone is vacuous).
+* STHOSVD (c3): the error against the oracle, and per-step parity with the oracle fed the GPU's own step
+  input (R16).
+* Factors: Q_nᵀQ_n = I within 1e-6.
+
+Tolerances (BASELINE north_star): per-mode relative Frobenius error of Y_n <= 1e-5."""
 import numpy as np
 import pytest
 import torch
@@ -16,7 +21,9 @@ import synth
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 Y_TOL = 1e-5
-ERR_TOL = 1e-4
+ERR_ABS = 1e-4
+ERR_REL = 1e-2
+QTQ_TOL = 1e-6
 
 
 @pytest.fixture(scope="module")
@@ -29,19 +36,11 @@ def krp():
     yield krp
 
 
-def _rows(I, rng):
-    return sorted(set([0, 1, I // 2, I - 1] + [int(v) for v in rng.integers(0, I, 2)]))
-
-
 def _rel(a, b):
     return float(np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b))
 
 
-@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
-def test_sketch_fullsize_sampled_rows(krp, name):
-    cfg = synth.config(name)
-    x = synth.tensor(cfg, 0)
-    om = synth.omegas(cfg.dims, cfg.R, 0)
+def _gpu_sketch(krp, cfg, x, om):
     dev = torch.device("cuda", 0)
     X = torch.from_numpy(x).to(dev)
     O = [torch.from_numpy(o).to(dev) for o in om]
@@ -49,68 +48,96 @@ def test_sketch_fullsize_sampled_rows(krp, name):
     Y = [torch.empty((n, cfg.R), dtype=torch.float32, device=dev) for n in cfg.dims]
     krp.krp_sketch_all_modes(X, cfg.dims, O, Y=Y, ws=ws)
     torch.cuda.synchronize()
-    del X
-    rng = np.random.default_rng(7)
+    out = [y.cpu().numpy() for y in Y]
+    del X, O, ws, Y
+    torch.cuda.empty_cache()
+    return out
+
+
+def _check_q(Q, ranks):
+    for q, r in zip(Q, ranks):
+        q = q.double().cpu().numpy()
+        dev = np.abs(q.T @ q - np.eye(r)).max()
+        assert dev <= QTQ_TOL, dev
+
+
+def _err_close(err, err_ref):
+    assert abs(err - err_ref) <= ERR_ABS, (err, err_ref)
+    assert abs(err - err_ref) <= ERR_REL * err_ref, (err, err_ref)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_sketch_fullsize_elementwise(krp, name):
+    cfg = synth.config(name)
+    x = synth.tensor(cfg, 0)
+    om = synth.omegas(cfg.dims, cfg.R, 0)
+    Y = _gpu_sketch(krp, cfg, x, om)
+    ref = oracle.sketch_all_modes(oracle.as_tensor(x, cfg.dims), om, chunk=max(1, cfg.dims[-1] // 8))
     for n in range(cfg.d):
-        Yh = Y[n].cpu().numpy()
-        assert np.isfinite(Yh).all()
-        rows = _rows(cfg.dims[n], rng)
-        ref = oracle.sketch_rows_ttv(x, cfg.dims, om, n, rows)
-        e = _rel(Yh[rows], ref)
+        assert np.isfinite(Y[n]).all()
+        e = _rel(Y[n], ref[n])
         assert e <= Y_TOL, (name, n, e)
 
 
-def test_rhosvd_fullsize_c2(krp):
-    cfg = synth.config("c2")
+def test_sketch_fullsize_c5_rows_in_every_block(krp):
+    cfg = synth.config("c5")
     x = synth.tensor(cfg, 0)
     om = synth.omegas(cfg.dims, cfg.R, 0)
-    _, _, err_ref, _ = oracle.rhosvd(oracle.as_tensor(x, cfg.dims), om, cfg.ranks, chunk=64)
+    Y = _gpu_sketch(krp, cfg, x, om)
+    rng = np.random.default_rng(7)
+    for n in range(cfg.d):
+        I = cfg.dims[n]
+        rows = []
+        for b0 in range(0, I, 128):  # two rows in every 128-row block (first + a random one)
+            b1 = min(I, b0 + 128)
+            rows += sorted({b0, int(rng.integers(b0, b1))})
+        ref = oracle.sketch_rows_ttv(x, cfg.dims, om, n, rows)
+        assert np.isfinite(Y[n]).all()
+        e = _rel(Y[n][rows], ref)
+        assert e <= Y_TOL, (n, e)
+        # and every sampled row on its own
+        for t, i in enumerate(rows):
+            assert _rel(Y[n][i], ref[t]) <= 10 * Y_TOL, (n, i)
+
+
+@pytest.mark.parametrize("name", ["c2", "c4", "c5"])
+def test_rhosvd_fullsize_vs_oracle(krp, name):
+    cfg = synth.config(name)
+    x = synth.tensor(cfg, 0)
+    om = synth.omegas(cfg.dims, cfg.R, 0)
     Q, core, err = krp.krp_rhosvd(torch.from_numpy(x).cuda(), cfg.dims, cfg.ranks,
                                   [torch.from_numpy(o).cuda() for o in om], with_error=True)
-    assert abs(err - err_ref) <= ERR_TOL, (err, err_ref)
-    for q, r in zip(Q, cfg.ranks):
-        q = q.double().cpu().numpy()
-        assert np.abs(q.T @ q - np.eye(r)).max() < 1e-4
+    _check_q(Q, cfg.ranks)
+    torch.cuda.empty_cache()
+    _, _, err_ref, _ = oracle.rhosvd(oracle.as_tensor(x, cfg.dims), om, cfg.ranks,
+                                     chunk=max(1, cfg.dims[-1] // 16))
+    _err_close(err, err_ref)
 
 
 def test_sthosvd_fullsize_c3(krp):
     cfg = synth.config("c3")
     x = synth.tensor(cfg, 0)
     oms = synth.sthosvd_omegas(cfg.dims, cfg.R, 0)
-    _, _, err_ref, _ = oracle.sthosvd(oracle.as_tensor(x, cfg.dims), oms, cfg.ranks)
     dom = [[None if o is None else torch.from_numpy(o).cuda() for o in row] for row in oms]
     Q, core, err = krp.krp_sthosvd(torch.from_numpy(x).cuda(), cfg.dims, cfg.ranks, dom, with_error=True)
-    assert abs(err - err_ref) <= ERR_TOL, (err, err_ref)
-
-
-@pytest.mark.parametrize("name", ["c4", "c5"])
-def test_rhosvd_fullsize_sampled_error(krp, name):
-    cfg = synth.config(name)
-    x = synth.tensor(cfg, 0)
-    om = synth.omegas(cfg.dims, cfg.R, 0)
-    Q, core, err = krp.krp_rhosvd(torch.from_numpy(x).cuda(), cfg.dims, cfg.ranks,
-                                  [torch.from_numpy(o).cuda() for o in om], with_error=True)
+    _check_q(Q, cfg.ranks)
+    _, _, err_ref, _ = oracle.sthosvd(oracle.as_tensor(x, cfg.dims), oms, cfg.ranks)
+    _err_close(err, err_ref)
+    # per-step parity (R16): the oracle sketches the GPU's own step input G^(i-1) = X x_1 Q_1^T .. x_{i-1} Q_{i-1}^T
+    d = cfg.d
     qs = [q.double().cpu().numpy() for q in Q]
-    for q, r in zip(qs, cfg.ranks):
-        assert np.abs(q.T @ q - np.eye(r)).max() < 1e-4
-    g = core.double().cpu().numpy().reshape(cfg.ranks, order="F")
-    rng = np.random.default_rng(3)
-    m = 1 << 18
-    idx = [rng.integers(0, n, m) for n in cfg.dims]
-    lin = np.zeros(m, dtype=np.int64)
-    stride = 1
-    for k, n in enumerate(cfg.dims):
-        lin += idx[k] * stride
-        stride *= n
-    xs = x[lin].astype(np.float64)
-    # X̂(i) = Σ_core g(c) Π_k Q_k(i_k, c_k), contracted mode by mode on chunks of sampled entries
-    xh = np.empty(m)
-    for c0 in range(0, m, 2048):
-        c1 = min(m, c0 + 2048)
-        t = np.einsum("...a,ma->m...", g, qs[cfg.d - 1][idx[cfg.d - 1][c0:c1]])
-        for k in range(cfg.d - 2, -1, -1):
-            t = np.einsum("m...a,ma->m...", t, qs[k][idx[k][c0:c1]])
-        xh[c0:c1] = t
-    est = float(np.sqrt(np.sum((xs - xh) ** 2) / np.sum(xs ** 2)))
-    # the Monte-Carlo estimate of a relative error has a few % spread at 2^18 samples
-    assert abs(est - err) <= 0.1 * err + 1e-7, (name, err, est)
+    G = oracle.as_tensor(x, cfg.dims)
+    cur = list(cfg.dims)
+    for i in range(d):
+        om_i = [None if j == i else (oms[i][j][:cfg.ranks[j]] if j < i else oms[i][j]) for j in range(d)]
+        gin = np.asarray(G).reshape(-1, order="F").astype(np.float32)
+        y_gpu = krp.krp_sketch_mode(torch.from_numpy(gin).cuda(), cur, i,
+                                    [None if o is None else torch.from_numpy(o).cuda() for o in om_i])
+        y_ref = oracle.sketch_mode(oracle.as_tensor(gin, cur), om_i, i)
+        assert _rel(y_gpu.cpu().numpy(), y_ref) <= Y_TOL, i
+        # the GPU's Q_i lies in the range of that step's sketch
+        u, sv, _ = np.linalg.svd(y_ref, full_matrices=False)
+        ub = u[:, sv > sv[0] * 1e-6]
+        assert np.linalg.norm(qs[i] - ub @ (ub.T @ qs[i])) / np.sqrt(cfg.ranks[i]) <= 1e-4, i
+        G = oracle.ttm(G, qs[i].T, i)
+        cur[i] = cfg.ranks[i]

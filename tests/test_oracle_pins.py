@@ -134,11 +134,11 @@ def test_sketch_integer_worked_example():
         assert np.array_equal(oracle.sketch_mode(x, om, n), expect), n
 
 
-@pytest.mark.parametrize("d", [3, 4])
+@pytest.mark.parametrize("d", [3, 4, 5])
 def test_rank_one_closed_form(d):
-    """BASELINE north_star pin (2): X = a∘b∘c => Y_1 = a·((bᵀΩ_2)∘(cᵀΩ_3)) columnwise."""
+    """BASELINE north_star pin (2): X = a∘b∘c => Y_1 = a·((bᵀΩ_2)∘(cᵀΩ_3)) columnwise (d = 3, 4, 5)."""
     g = _rng(10 + d)
-    dims = (5, 4, 3, 2)[:d]
+    dims = (5, 4, 3, 2, 3)[:d]
     vecs = [g.standard_normal(n) for n in dims]
     x = vecs[0]
     for v in vecs[1:]:
@@ -446,3 +446,22 @@ def test_sampled_rows_ttv_matches_explicit_kr(dims):
         ref = oracle.sketch_mode(x, om, n)
         got = oracle.sketch_rows_ttv(flat, dims, om, n, list(range(dims[n])))
         assert np.allclose(got, ref, rtol=1e-12, atol=1e-12), n
+
+
+def test_chunked_rhosvd_and_error_match_unchunked():
+    """Memory-only chunking (last-mode slabs) changes the fp64 summation order, never the terms: the chunked
+    sketch, core and Tucker error of rhosvd equal the unchunked ones to rounding (pins the chunked branches
+    of sketch_mode, _core_slabwise and tucker_error that the full-size GPU tests use)."""
+    cfg = synth.config("c2").scaled((24, 20, 18))
+    x = oracle.as_tensor(synth.tensor(cfg, 4), cfg.dims)
+    om = synth.omegas(cfg.dims, cfg.R if cfg.R <= 18 else 12, 4)
+    ranks = (5, 5, 5)
+    q0, g0, e0, y0 = oracle.rhosvd(x, om, ranks, chunk=None)
+    for chunk in (1, 5, 7, 17):
+        q1, g1, e1, y1 = oracle.rhosvd(x, om, ranks, chunk=chunk)
+        for a, b in zip(y0, y1):
+            assert np.allclose(a, b, rtol=1e-12, atol=1e-12 * np.abs(a).max())
+        assert abs(e1 - e0) <= 1e-12
+        assert np.allclose(np.abs(g1), np.abs(g0), rtol=1e-9, atol=1e-12)
+        # the chunked error of the same decomposition equals the unchunked one
+        assert abs(oracle.tucker_error(x, g0, q0, chunk=chunk) - e0) <= 1e-13
