@@ -134,6 +134,14 @@ KRP_API int krp_sketch_all_modes_dist(const float* X_slab, int d, const int64_t*
 KRP_API int krp_rhosvd_dist(const float* X_slab, int d, const int64_t* dims_local, int64_t I_d_global, int64_t slab_begin,
                     const int* ranks, int R, const float* const* omega, float* const* Q, float* core,
                     double* rel_err, void* ws, size_t ws_bytes, krp_comm comm, void* stream);
+/* RSTHOSVD-KRP (Alg. 8) on a slab-sharded tensor: steps i < d-1 keep the slab
+ * layout (the step sketch and the mode Gram of B_(i) are all-reduced, the TTMs are local); the last step
+ * gathers the complete rows of Y_d with the zero-padded all-reduce, contracts the sharded mode locally and
+ * all-reduces the partial core.  omega[i*d + j] as in krp_sthosvd, with the GLOBAL I_d rows for j = d-1;
+ * Q[d-1] is the global I_d x r_d factor; Q, core and rel_err are replicated on every rank. */
+KRP_API int krp_sthosvd_dist(const float* X_slab, int d, const int64_t* dims_local, int64_t I_d_global,
+                             int64_t slab_begin, const int* ranks, int R, const float* const* omega, float* const* Q,
+                             float* core, double* rel_err, void* ws, size_t ws_bytes, krp_comm comm, void* stream);
 /* Host-side sharding geometry (pure host functions, no device access; used by the _dist calls and by
  * callers that place the slabs).  SURVEY §8(e): rank g of G owns the contiguous last-mode index range
  * [begin, begin + len) with begin = floor(g * I_d / G) (balanced, ragged when G does not divide I_d).

@@ -23,6 +23,7 @@ __all__ = [
     "OP_RHOSVD_ERR", "krp_workspace_bytes",
     "krp_sketch_all_modes", "krp_sketch_all_modes_host", "krp_sketch_mode", "krp_rhosvd", "krp_sthosvd",
     "krp_launch_count", "krp_reset_launch_count", "Comm", "krp_sketch_all_modes_dist", "krp_rhosvd_dist",
+    "krp_sthosvd_dist",
     "krp_workspace_bytes_dist", "EXPORTED_SYMBOLS", "LIB_PATH", "krp_slab_range", "krp_pack_layout",
 ]
 
@@ -34,7 +35,7 @@ EXPORTED_SYMBOLS = [
     "krp_status_string", "krp_last_error_message", "krp_version", "krp_workspace_bytes",
     "krp_sketch_all_modes", "krp_sketch_all_modes_host", "krp_sketch_mode", "krp_rhosvd", "krp_sthosvd",
     "krp_comm_id_bytes", "krp_comm_get_unique_id", "krp_comm_init", "krp_comm_destroy",
-    "krp_sketch_all_modes_dist", "krp_rhosvd_dist", "krp_workspace_bytes_dist", "krp_launch_count",
+    "krp_sketch_all_modes_dist", "krp_rhosvd_dist", "krp_sthosvd_dist", "krp_workspace_bytes_dist", "krp_launch_count",
     "krp_reset_launch_count", "krp_profile_enable", "krp_profile_read", "krp_profile_reset",
     "krp_slab_range", "krp_pack_layout",
 ]
@@ -86,6 +87,7 @@ def lib() -> ctypes.CDLL:
                                                  ctypes.c_int, ptrs, _P, ctypes.c_size_t, _P, _P]
         l_.krp_rhosvd_dist.argtypes = [_P, ctypes.c_int, _I64P, ctypes.c_int64, ctypes.c_int64, _IP, ctypes.c_int,
                                        ptrs, ptrs, _P, ctypes.POINTER(ctypes.c_double), _P, ctypes.c_size_t, _P, _P]
+        l_.krp_sthosvd_dist.argtypes = l_.krp_rhosvd_dist.argtypes
         l_.krp_slab_range.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int, _I64P, _I64P]
         l_.krp_pack_layout.argtypes = [ctypes.c_int, _I64P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, _I64P, _I64P]
         l_.krp_launch_count.restype = ctypes.c_uint64
@@ -331,4 +333,24 @@ def krp_rhosvd_dist(X_slab: torch.Tensor, dims_local: Sequence[int], I_d_global:
                                  int(slab_begin), _ints(ranks), R, _ptr_array(omegas), _ptr_array(Q), core.data_ptr(),
                                  ctypes.byref(err) if with_error else None, w.data_ptr(), w.numel(), comm.handle,
                                  _stream(stream)), "krp_rhosvd_dist")
+    return Q, core, (err.value if with_error else None)
+
+
+def krp_sthosvd_dist(X_slab: torch.Tensor, dims_local: Sequence[int], I_d_global: int, slab_begin: int,
+                     ranks: Sequence[int], omegas: Sequence[Sequence[Optional[torch.Tensor]]], comm: Comm,
+                     with_error: bool = False, ws=None, stream=None):
+    """Slab-sharded RSTHOSVD-KRP (Alg. 8); omegas[i][j] as in krp_sthosvd with the GLOBAL I_d rows for j = d-1."""
+    _dev_f32(X_slab, "X_slab")
+    d = len(dims_local)
+    R = int(omegas[0][1].shape[1])
+    flat = [omegas[i][j] for i in range(d) for j in range(d)]
+    gdims = list(dims_local[:-1]) + [int(I_d_global)]
+    Q = [torch.empty((int(n), int(r)), dtype=torch.float32, device=X_slab.device) for n, r in zip(gdims, ranks)]
+    core = torch.empty(int(torch.tensor(list(ranks)).prod()), dtype=torch.float32, device=X_slab.device)
+    err = ctypes.c_double(0.0)
+    w = _ws(krp_workspace_bytes_dist(OP_STHOSVD, dims_local, I_d_global, R, ranks), X_slab.device, ws)
+    _check(lib().krp_sthosvd_dist(X_slab.data_ptr(), d, _dims(dims_local), int(I_d_global), int(slab_begin),
+                                  _ints(ranks), R, _ptr_array(flat), _ptr_array(Q), core.data_ptr(),
+                                  ctypes.byref(err) if with_error else None, w.data_ptr(), w.numel(), comm.handle,
+                                  _stream(stream)), "krp_sthosvd_dist")
     return Q, core, (err.value if with_error else None)

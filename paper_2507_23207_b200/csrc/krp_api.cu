@@ -530,18 +530,28 @@ static int rhosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_t
 }
 
 // ================================================================== STHOSVD
-static int sthosvd_impl(const float* X, const Dims& g, const int* ranks, int R, const float* const* omega,
-                        float* const* Q, float* core, double* rel_err, Arena& ar, cudaStream_t s, bool measure_only) {
+// RSTHOSVD-KRP (Alg. 8) on a (possibly slab-sharded) tensor.  g = local dims (the last mode is the
+// local slab [slab_begin, slab_begin + g.n[d-1]) of Id_global rows); dc != nullptr combines across ranks
+// (SURVEY §8(e)): steps i < d-1 keep the slab layout — their sketch and the mode Gram of B_(i) are sums over
+// slabs (all-reduce) and the TTMs are local; the last step sketches complete rows of Y_d, gathered by the
+// zero-padded all-reduce, contracts the sharded mode locally and all-reduces the (small) partial core.
+static int sthosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_t slab_begin, const int* ranks, int R,
+                        const float* const* omega, float* const* Q, float* core, double* rel_err, Arena& ar,
+                        cudaStream_t s, DistCtx* dc, bool measure_only) {
   const int d = g.d;
+  const bool dist = dc != nullptr;
+  int64_t gd[kMaxD];  // global dims
+  for (int k = 0; k < d; ++k) gd[k] = g.n[k];
+  gd[d - 1] = Id_global;
   int64_t imax = 0;
-  for (int k = 0; k < d; ++k) imax = std::max(imax, g.n[k]);
+  for (int k = 0; k < d; ++k) imax = std::max(imax, gd[k]);
   float* Y = ar.take<float>(imax * R);
   float* Qf = ar.take<float>(imax * R);
   double* H = ar.take<double>(static_cast<size_t>(R) * R);
   float* U = ar.take<float>(static_cast<size_t>(R) * R);
   int* flag = ar.take<int>(4);
   double* errsum = ar.take<double>(2);
-  // step buffers: B_i = G x_i Q^T has dims (r_<i, R, I_>i); G_i has (r_<=i, I_>i)
+  // step buffers: B_i = G x_i Q^T has dims (r_<i, R, I_>i); G_i has (r_<=i, I_>i)  (local last mode)
   int64_t bmax = 0;
   for (int i = 0; i < d; ++i) {
     int64_t b = 1;
@@ -559,13 +569,13 @@ static int sthosvd_impl(const float* X, const Dims& g, const int* ranks, int R, 
       bool want[kMaxD] = {};
       want[i] = true;
       scratch = std::max(scratch, sketch_ws_bytes(cg, R, want));
-      scratch = std::max(scratch, cholqr_ws_bytes(g.n[i], R));
+      scratch = std::max(scratch, cholqr_ws_bytes(gd[i], R));
       cur[i] = R;
       scratch = std::max(scratch, mode_gram_ws_bytes(make_dims(d, cur), i));
       cur[i] = ranks[i];
     }
   }
-  // error pass (full reconstruction, chunked over the last mode) reuses B/GA-sized buffers
+  // error pass (full reconstruction of the local slab, chunked over the last mode) reuses B/GA-sized buffers
   const int64_t inner = g.N / g.n[d - 1];
   int64_t chunk = std::max<int64_t>(1, (int64_t(1) << 25) / std::max<int64_t>(inner, 1));
   chunk = std::min<int64_t>(chunk, g.n[d - 1]);
@@ -598,41 +608,55 @@ static int sthosvd_impl(const float* X, const Dims& g, const int* ranks, int R, 
   for (int k = 0; k < d; ++k) cur[k] = g.n[k];
   const float* G = X;
   for (int i = 0; i < d; ++i) {
+    const bool last = i == d - 1;
     const Dims cg = make_dims(d, cur);
-    // 1. Y_i = G_(i) (⊙_{j != i} Omega^{(i)}_j), compressed modes read only their leading r_j rows
+    // 1. Y_i = G_(i) (⊙_{j != i} Omega^{(i)}_j), compressed modes read only their leading r_j rows; the
+    //    sharded mode reads its slab rows
     OmegaPtrs om{};
     for (int j = 0; j < d; ++j) om.p[j] = (j == i) ? nullptr : omega[i * d + j];
+    if (dist && !last) om.p[d - 1] = omega[i * d + d - 1] + slab_begin * R;
     bool want[kMaxD] = {};
     want[i] = true;
     float* Yp[kMaxD] = {};
-    Yp[i] = Y;
+    const int64_t yrows = last ? gd[d - 1] : cur[i];
+    if (dist && last) {  // complete local rows of Y_d at their global offset, zero elsewhere: the sum gathers
+      KRP_CHECK_CUDA(cudaMemsetAsync(Y, 0, yrows * R * sizeof(float), s));
+      Yp[i] = Y + slab_begin * R;
+    } else {
+      Yp[i] = Y;
+    }
     KRP_TRY(sketch(G, cg, om, R, want, Yp, ar, s));
     ar.off = mark;
-    // 2. thin QR
-    KRP_TRY(cholqr(Y, cur[i], R, Qf, nullptr, flag, ar, s));
+    if (dist) KRP_TRY(allreduce_sum_f32(dc, Y, static_cast<size_t>(yrows * R), s));
+    // 2. thin QR, replicated
+    KRP_TRY(cholqr(Y, yrows, R, Qf, nullptr, flag, ar, s));
     ar.off = mark;
-    // 3. B = G x_i Q^T
-    KRP_TRY(ttm(G, cg, i, Qf, R, 1, R, B, s));
+    // 3. B = G x_i Q^T: local; on the sharded mode the slab rows of Q, and the partial B is summed
+    const float* Qrows = (dist && last) ? Qf + slab_begin * R : Qf;
+    KRP_TRY(ttm(G, cg, i, Qrows, R, 1, R, B, s));
     int64_t bd[kMaxD];
     for (int k = 0; k < d; ++k) bd[k] = cur[k];
     bd[i] = R;
     const Dims bg = make_dims(d, bd);
-    float* Gout = (i == d - 1) ? core : GA;
+    if (dist && last) KRP_TRY(allreduce_sum_f32(dc, B, static_cast<size_t>(bg.N), s));
+    float* Gout = last ? core : GA;
     if (ranks[i] < R) {
-      // 4. U = leading r_i left singular vectors of B_(i); G <- B x_i U^T; Q_i = Q U
+      // 4. U = leading r_i left singular vectors of B_(i) (its Gram sums over the slabs for i < d-1);
+      //    G <- B x_i U^T; Q_i = Q U
       KRP_TRY(mode_gram(B, bg, i, H, ar, s));
       ar.off = mark;
+      if (dist && !last) KRP_TRY(allreduce_sum_f64(dc, H, static_cast<size_t>(R) * R, s));
       KRP_TRY(sym_eig_top(H, R, ranks[i], U, s));
       KRP_TRY(ttm(B, bg, i, U, ranks[i], 1, ranks[i], Gout, s));
-      int64_t qd[2] = {R, cur[i]};
+      int64_t qd[2] = {R, yrows};
       KRP_TRY(ttm(Qf, make_dims(2, qd), 0, U, ranks[i], 1, ranks[i], Q[i], s));
     } else {
       KRP_CHECK_CUDA(cudaMemcpyAsync(Gout, B, bg.N * sizeof(float), cudaMemcpyDeviceToDevice, s));
-      KRP_CHECK_CUDA(cudaMemcpyAsync(Q[i], Qf, cur[i] * R * sizeof(float), cudaMemcpyDeviceToDevice, s));
+      KRP_CHECK_CUDA(cudaMemcpyAsync(Q[i], Qf, yrows * R * sizeof(float), cudaMemcpyDeviceToDevice, s));
     }
     cur[i] = ranks[i];
     // the next step reads GA (B is free again: it is rewritten from GA before GA is overwritten)
-    if (i < d - 1) G = GA;
+    if (!last) G = GA;
   }
   if (rel_err) {
     KRP_CHECK_CUDA(cudaMemsetAsync(errsum, 0, 2 * sizeof(double), s));
@@ -640,8 +664,8 @@ static int sthosvd_impl(const float* X, const Dims& g, const int* ranks, int R, 
     for (int k = 0; k < d; ++k) cd[k] = ranks[k];
     for (int64_t k0 = 0; k0 < g.n[d - 1]; k0 += chunk) {
       const int64_t k1 = std::min<int64_t>(g.n[d - 1], k0 + chunk);
-      KRP_TRY(ttm(core, make_dims(d, cd), d - 1, Q[d - 1] + k0 * ranks[d - 1], static_cast<int>(k1 - k0),
-                  ranks[d - 1], 1, EA, s));
+      KRP_TRY(ttm(core, make_dims(d, cd), d - 1, Q[d - 1] + (slab_begin + k0) * ranks[d - 1],
+                  static_cast<int>(k1 - k0), ranks[d - 1], 1, EA, s));
       int64_t ed[kMaxD];
       for (int m = 0; m < d; ++m) ed[m] = cd[m];
       ed[d - 1] = k1 - k0;
@@ -655,6 +679,7 @@ static int sthosvd_impl(const float* X, const Dims& g, const int* ranks, int R, 
       KRP_TRY(sqdiff_accumulate(X + k0 * inner, Xh, (k1 - k0) * inner, errsum, ar, s));
       ar.off = mark;
     }
+    if (dist) KRP_TRY(allreduce_sum_f64(dc, errsum, 2, s));
   }
   int hflag[4] = {0, 0, 0, 0};
   double herr[2] = {0.0, 0.0};
@@ -765,7 +790,7 @@ static size_t ws_bytes_impl(int op, int d, const int64_t* dims, int64_t Id_globa
     case KRP_OP_STHOSVD: {
       if (!ranks) return 0;
       double dummy;
-      sthosvd_impl(nullptr, g, ranks, R, nullptr, nullptr, nullptr, &dummy, ar, nullptr, true);
+      sthosvd_impl(nullptr, g, Id_global, 0, ranks, R, nullptr, nullptr, nullptr, &dummy, ar, nullptr, nullptr, true);
       return ar.off + 256;
     }
     default:
@@ -902,7 +927,7 @@ int krp_sthosvd(const float* X, int d, const int64_t* dims, const int* ranks, in
   Arena ar;
   WsGuard guard;
   KRP_TRY(setup_arena(krp_workspace_bytes(KRP_OP_STHOSVD, d, dims, R, ranks), ws, ws_bytes, s, ar, guard));
-  return sthosvd_impl(X, g, ranks, R, omega, Q, core, rel_err, ar, s, false);
+  return sthosvd_impl(X, g, dims[d - 1], 0, ranks, R, omega, Q, core, rel_err, ar, s, nullptr, false);
 }
 
 // ------------------------------------------------------------------ distributed
@@ -1044,6 +1069,39 @@ int krp_sketch_all_modes_dist(const float* X_slab, int d, const int64_t* dims_lo
     KRP_CHECK_CUDA(cudaMemcpyAsync(Y[k], pack + poff[k], (poff[k + 1] - poff[k]) * sizeof(float),
                                    cudaMemcpyDeviceToDevice, s));
   return KRP_OK;
+}
+
+int krp_sthosvd_dist(const float* X_slab, int d, const int64_t* dims_local, int64_t I_d_global, int64_t slab_begin,
+                     const int* ranks, int R, const float* const* omega, float* const* Q, float* core,
+                     double* rel_err, void* ws, size_t ws_bytes, krp_comm comm, void* stream) {
+  KRP_TRY(validate_common(X_slab, d, dims_local, R));
+  KRP_TRY(validate_slab(d, dims_local, I_d_global, slab_begin));
+  if (!omega) {
+    set_error("omega is NULL");
+    return KRP_EINVAL;
+  }
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j)
+      if (i != j && !omega[i * d + j]) {
+        set_error("omega[%d*d+%d] is NULL", i, j);
+        return KRP_EINVAL;
+      }
+  KRP_TRY(validate_ptrs(Q, d, -1, "Q"));
+  if (!core || !comm) {
+    set_error("core/comm is NULL");
+    return KRP_EINVAL;
+  }
+  int64_t gd[kMaxD];
+  for (int k = 0; k < d; ++k) gd[k] = dims_local[k];
+  gd[d - 1] = I_d_global;
+  KRP_TRY(validate_ranks(make_dims(d, gd), ranks, R));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const Dims g = make_dims(d, dims_local);
+  Arena ar;
+  WsGuard guard;
+  KRP_TRY(setup_arena(krp_workspace_bytes_dist(KRP_OP_STHOSVD, d, dims_local, I_d_global, R, ranks), ws, ws_bytes, s,
+                      ar, guard));
+  return sthosvd_impl(X_slab, g, I_d_global, slab_begin, ranks, R, omega, Q, core, rel_err, ar, s, &comm->ctx, false);
 }
 
 int krp_rhosvd_dist(const float* X_slab, int d, const int64_t* dims_local, int64_t I_d_global, int64_t slab_begin,

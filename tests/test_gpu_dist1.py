@@ -101,6 +101,23 @@ def test_dist_rhosvd_whole_tensor_equals_single_gpu(env):
     assert abs(e2 - eref) <= 1e-4, (e2, eref)
 
 
+def test_dist_sthosvd_whole_tensor_matches_oracle(env):
+    """krp_sthosvd_dist with the whole tensor as one slab: the single-GPU decomposition and the oracle's error."""
+    krp, comm = env
+    cfg = synth.config("c3").scaled((24, 20, 18, 16))
+    x = synth.tensor(cfg, 5)
+    oms = synth.sthosvd_omegas(cfg.dims, cfg.R, 5)
+    dom = [[None if o is None else _dev(o) for o in row] for row in oms]
+    _, _, e1 = krp.krp_sthosvd(_dev(x), cfg.dims, cfg.ranks, dom, with_error=True)
+    Q, core, e2 = krp.krp_sthosvd_dist(_dev(x), cfg.dims, cfg.dims[-1], 0, cfg.ranks, dom, comm, with_error=True)
+    assert abs(e1 - e2) <= 1e-7 * max(1.0, abs(e1)), (e1, e2)
+    _, _, eref, _ = oracle.sthosvd(oracle.as_tensor(x, cfg.dims), oms, cfg.ranks)
+    assert abs(e2 - eref) <= 1e-4, (e2, eref)
+    for q, r in zip(Q, cfg.ranks):
+        qq = q.double().cpu().numpy()
+        assert np.abs(qq.T @ qq - np.eye(r)).max() <= 1e-6
+
+
 def _nccl_worker(rank, world, port, q):
     """One rank of a 2-GPU run: sketch the rank's slab with the NCCL combine, compare with the oracle."""
     try:
@@ -123,6 +140,18 @@ def _nccl_worker(rank, world, port, q):
         torch.cuda.synchronize()
         ref = oracle.sketch_all_modes(oracle.as_tensor(x, dims), om_np)
         err = max(float(np.linalg.norm(y.double().cpu().numpy() - r) / np.linalg.norm(r)) for y, r in zip(Y, ref))
+        # sharded STHOSVD (Alg. 8) of a Tucker tensor vs the oracle's error
+        cfg = synth.config("c3").scaled((24, 20, 18, 16))
+        xt = synth.tensor(cfg, 6)
+        oms = synth.sthosvd_omegas(cfg.dims, cfg.R, 6)
+        b2, n2 = krp.krp_slab_range(cfg.dims[-1], world, rank)
+        inn = int(np.prod(cfg.dims[:-1]))
+        dom = [[None if o is None else _dev(o) for o in row] for row in oms]
+        _, _, es = krp.krp_sthosvd_dist(_dev(xt[b2 * inn:(b2 + n2) * inn]), list(cfg.dims[:-1]) + [n2],
+                                        cfg.dims[-1], b2, cfg.ranks, dom, comm, with_error=True)
+        _, _, eref, _ = oracle.sthosvd(oracle.as_tensor(xt, cfg.dims), oms, cfg.ranks)
+        if abs(es - eref) > 1e-4:
+            err = max(err, 1.0)
         comm.close()
         dist.destroy_process_group()
         q.put((rank, err))
