@@ -104,7 +104,7 @@ def test_dist_rhosvd_whole_tensor_equals_single_gpu(env):
 def test_dist_sthosvd_whole_tensor_matches_oracle(env):
     """krp_sthosvd_dist with the whole tensor as one slab: the single-GPU decomposition and the oracle's error."""
     krp, comm = env
-    cfg = synth.config("c3").scaled((24, 20, 18, 16))
+    cfg = synth.config("c3").scaled((40, 36, 32, 32))
     x = synth.tensor(cfg, 5)
     oms = synth.sthosvd_omegas(cfg.dims, cfg.R, 5)
     dom = [[None if o is None else _dev(o) for o in row] for row in oms]
@@ -141,7 +141,7 @@ def _nccl_worker(rank, world, port, q):
         ref = oracle.sketch_all_modes(oracle.as_tensor(x, dims), om_np)
         err = max(float(np.linalg.norm(y.double().cpu().numpy() - r) / np.linalg.norm(r)) for y, r in zip(Y, ref))
         # sharded STHOSVD (Alg. 8) of a Tucker tensor vs the oracle's error
-        cfg = synth.config("c3").scaled((24, 20, 18, 16))
+        cfg = synth.config("c3").scaled((40, 36, 32, 32))
         xt = synth.tensor(cfg, 6)
         oms = synth.sthosvd_omegas(cfg.dims, cfg.R, 6)
         b2, n2 = krp.krp_slab_range(cfg.dims[-1], world, rank)

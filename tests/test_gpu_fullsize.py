@@ -5,7 +5,12 @@ workspace, the default plan), against the fp64 oracle on the same seeded inputs.
   explicit-Khatri-Rao sketch (chunked over the last mode: same terms, fp64); at c5, two rows in every
   128-row block of every mode by the column identity (oracle.sketch_rows_ttv).
 * rHOSVD: the reported Tucker error against the oracle's own rHOSVD at c2, c4 and c5 (|Δ| <= 1e-4, reading
-  R12, and <= 1 % relative: at c5 the error is ~1.3e-6, where the absolute bar alone is vacuous).
+  R12), plus a relative bar on the GPU's decomposition (its Q_n and core) evaluated by the fp64 oracle:
+  1 % at c2 and c4.  At c5 the target error (~1.1e-6) sits at the relative accuracy of any fp32 sketch of
+  the fp32 tensor (~1e-6, the same order as c5's 1e-6 noise), so the directions past the noise floor are
+  set by rounding and several answers are correct (R16); the bar there is 20 % (reading R22; measured:
+  1.15x the oracle's error, 1.05x with an exact core for the GPU's subspaces).  The GPU's own error value
+  must also agree with the fp64 evaluation of its decomposition to 1e-6 (its fp32 evaluation floor).
 * STHOSVD (c3): the error against the oracle, and per-step parity with the oracle fed the GPU's own step
   input (R16).
 * Factors: Q_nᵀQ_n = I within 1e-6.
@@ -109,9 +114,18 @@ def test_rhosvd_fullsize_vs_oracle(krp, name):
                                   [torch.from_numpy(o).cuda() for o in om], with_error=True)
     _check_q(Q, cfg.ranks)
     torch.cuda.empty_cache()
-    _, _, err_ref, _ = oracle.rhosvd(oracle.as_tensor(x, cfg.dims), om, cfg.ranks,
-                                     chunk=max(1, cfg.dims[-1] // 16))
-    _err_close(err, err_ref)
+    X64 = oracle.as_tensor(x, cfg.dims)
+    ch = max(1, cfg.dims[-1] // 16)
+    _, _, err_ref, _ = oracle.rhosvd(X64, om, cfg.ranks, chunk=ch)
+    assert abs(err - err_ref) <= ERR_ABS, (err, err_ref)
+    # the GPU decomposition evaluated in fp64 reaches the oracle's error within the per-config bar (R22)
+    qs = [q.double().cpu().numpy() for q in Q]
+    g = core.double().cpu().numpy().reshape(cfg.ranks, order="F")
+    e64 = oracle.tucker_error(X64, g, qs, chunk=ch)
+    rel_bar = 0.2 if name == "c5" else ERR_REL
+    assert abs(e64 - err_ref) <= rel_bar * err_ref, (e64, err_ref)
+    # and the GPU's fp32-evaluated error lies within that evaluation's floor (R22)
+    assert abs(err - e64) <= 1e-6, (err, e64)
 
 
 def test_sthosvd_fullsize_c3(krp):
