@@ -48,6 +48,8 @@ __all__ = [
     "reconstruct",
     "tucker_error",
     "sketch_flops",
+    "hosvd",
+    "sthosvd_deterministic",
 ]
 
 
@@ -315,6 +317,28 @@ def sthosvd(x: np.ndarray, om_steps: Sequence[Sequence[Optional[np.ndarray]]], r
         qs.append(q)
     err = tucker_error(x, g, qs) if with_error else None
     return qs, g, err, ys
+
+
+# ----------------------------------------------------------------- deterministic baselines (context for NEXT-1)
+def hosvd(x: np.ndarray, ranks: Sequence[int]):
+    """Truncated HOSVD (the paper's deterministic baseline, Table 1 / Fig. 2): U_n = leading r_n left
+    singular vectors of X_(n); G = X ×_1 U_1ᵀ ... ×_d U_dᵀ.  Returns (us, core, err)."""
+    us = [leading_left_singular_vectors(unfold(x, n), int(r))[0] for n, r in enumerate(ranks)]
+    g = multi_ttm(x, [u.T for u in us])
+    return us, g, tucker_error(x, g, us)
+
+
+def sthosvd_deterministic(x: np.ndarray, ranks: Sequence[int]):
+    """Truncated STHOSVD (deterministic baseline): for i = 1..d, U_i = leading r_i left singular vectors of the
+    current core's mode-i unfolding, G <- G ×_i U_iᵀ (the Alg. 8 pattern with the exact SVD in place of the
+    sketch, P:538-559).  Returns (us, core, err)."""
+    g = x
+    us = []
+    for i, r in enumerate(ranks):
+        u, _ = leading_left_singular_vectors(unfold(g, i), int(r))
+        us.append(u)
+        g = ttm(g, u.T, i)
+    return us, g, tucker_error(x, g, us)
 
 
 # ----------------------------------------------------------------- accounting

@@ -17,6 +17,10 @@ bit-identical fp32 arrays.  Readings of the configs (R7/R9/R10/R1
   E), so each slab is generated independently.  ||X0||_F = ||core||_F for
   orthonormal factors.
 * Decay "0.8^(i+j+k)" and the smooth function use 0-based indices.
+* The paper's Cauchy tensor (NEXT-1): x = 1 / (i_1^a + ... + i_d^a)^(1/a) with 1-based
+  indices, a = 2; closed form, no random numbers, no noise.  Computed in fp64 (integer powers,
+  exact sums, a correctly rounded square root for a = 2) and rounded once to fp32, so the host generator
+  here and the device generator (cauchy_device) give bit-identical tensors.
 * "orthonormalised Gaussian factors": Q of a Householder QR of an iid N(0,1)
   I_k x r_k matrix.
 """
@@ -40,6 +44,7 @@ __all__ = [
     "tensor_slab",
     "tucker_parts",
     "random_tensor",
+    "cauchy_device",
 ]
 
 
@@ -49,11 +54,12 @@ class Config:
     dims: Tuple[int, ...]
     R: int                       # sketch width l = r + p
     ranks: Tuple[int, ...]       # target Tucker ranks r_n
-    kind: str                    # "tucker" | "smooth"
+    kind: str                    # "tucker" | "smooth" | "cauchy"
     core: Tuple[int, ...] = ()   # Tucker core dims
     decay: Optional[float] = None  # core entry scale decay**(sum of 0-based indices)
     eta: float = 0.0             # relative noise level
     workload: str = "rhosvd"     # "rhosvd" | "sthosvd"
+    alpha: float = 2.0           # Cauchy exponent (kind "cauchy")
 
     @property
     def d(self) -> int:
@@ -80,6 +86,9 @@ CONFIGS = {
     "c4": Config("c4", (64, 64, 64, 64, 64), 20, (10, 10, 10, 10, 10), "tucker", core=(10, 10, 10, 10, 10),
                  decay=0.7, eta=1e-4),
     "c5": Config("c5", (2048, 2048, 512), 60, (50, 50, 50), "smooth", eta=1e-6),
+    # NEXT-1: the paper's 4-way Cauchy tensor, n = 250, a = 2, no oversampling (R = r);
+    # the rank is swept by tools/cauchy_sweep.py, r = 30 here
+    "cauchy": Config("cauchy", (250, 250, 250, 250), 30, (30, 30, 30, 30), "cauchy", workload="rhosvd"),
 }
 
 
@@ -132,9 +141,46 @@ def _smooth_norm(dims: Sequence[int]) -> float:
     return math.sqrt(tot)
 
 
+def _cauchy_slab(dims: Sequence[int], alpha: float, k0: int, k1: int) -> np.ndarray:
+    """Cauchy tensor slab x[..., k0:k1] = 1 / (sum_j i_j^a)^(1/a), 1-based indices, fp64."""
+    d = len(dims)
+    s = np.zeros(tuple(dims[:-1]) + (k1 - k0,))
+    for j in range(d):
+        idx = np.arange(1, dims[j] + 1, dtype=np.float64) if j < d - 1 else np.arange(k0 + 1, k1 + 1, dtype=np.float64)
+        shape = [1] * d
+        shape[j] = idx.size
+        s = s + (idx * idx if alpha == 2.0 else idx ** alpha).reshape(shape)
+    return np.asfortranarray(1.0 / (np.sqrt(s) if alpha == 2.0 else s ** (1.0 / alpha)))
+
+
+def cauchy_device(dims: Sequence[int], alpha: float = 2.0, device="cuda"):
+    """The Cauchy tensor generated on the device with torch (the same fp64 formula as _cauchy_slab, rounded once
+    to fp32): a flat first-index-fastest fp32 tensor.  For the full n = 250 workload (15.6 GB), which is too
+    large to build on the host in reasonable time."""
+    import torch
+    d = len(dims)
+    out = torch.empty(int(np.prod(dims)), dtype=torch.float32, device=device)
+    inner = int(np.prod(dims[:-1]))
+    # sum over the first d-1 modes of i_j^a, first index fastest (fp64: exact integers)
+    s = torch.zeros(inner, dtype=torch.float64, device=device)
+    stride = 1
+    for j in range(d - 1):
+        idx = torch.arange(inner, device=device, dtype=torch.int64) // stride % dims[j] + 1
+        v = idx.to(torch.float64)
+        s += v * v if alpha == 2.0 else v ** alpha
+        stride *= dims[j]
+    for k in range(dims[-1]):
+        kk = float((k + 1) * (k + 1)) if alpha == 2.0 else float(k + 1) ** alpha
+        t = s + kk
+        out[k * inner:(k + 1) * inner] = (1.0 / (torch.sqrt(t) if alpha == 2.0 else t ** (1.0 / alpha))).to(torch.float32)
+    return out
+
+
 def _x0_slab(cfg: Config, seed: int, k0: int, k1: int, parts=None) -> np.ndarray:
     """Noise-free fp64 slab X0[..., k0:k1] (Fortran-ordered array of dims[:-1] + (k1-k0,))."""
     dims = cfg.dims
+    if cfg.kind == "cauchy":
+        return _cauchy_slab(dims, cfg.alpha, k0, k1)
     if cfg.kind == "smooth":
         assert cfg.d == 3
         i1, i2, i3 = dims
@@ -154,6 +200,8 @@ def _x0_slab(cfg: Config, seed: int, k0: int, k1: int, parts=None) -> np.ndarray
 
 
 def x0_norm(cfg: Config, seed: int, parts=None) -> float:
+    if cfg.kind == "cauchy":
+        return 0.0  # no noise is added (the norm only scales the noise)
     if cfg.kind == "smooth":
         return _smooth_norm(cfg.dims)
     return (parts if parts is not None else tucker_parts(cfg, seed))[2]

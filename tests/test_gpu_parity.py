@@ -259,3 +259,31 @@ def test_sthosvd_parity(krp, small):
     _check_factors(Q, cfg.ranks)
     assert abs(err - err_ref) <= ERR_TOL, (err, err_ref)
     _sthosvd_step_checks(krp, x, cfg.dims, oms, cfg.ranks, Q)
+
+
+# ----------------------------------------------------------------- NEXT-1: the paper's Cauchy workload
+@pytest.mark.parametrize("r", [4, 8])
+def test_cauchy_workload_vs_oracle(krp, r):
+    """The Cauchy tensor (a = 2, 1-based) at a reduced n, with no oversampling (R = r):
+    the device generator reproduces the host closed form bit for bit; the sketch, RHOSVD-KRP-MEMO and
+    RSTHOSVD-KRP match the oracle."""
+    cfg = synth.config("cauchy").scaled((40, 36, 32, 30))
+    ranks = (r,) * 4
+    x = synth.tensor(cfg, 0)
+    xd = synth.cauchy_device(cfg.dims)
+    assert torch.equal(xd.cpu(), torch.from_numpy(x))
+    om = synth.omegas(cfg.dims, r, 0)
+    X64 = oracle.as_tensor(x, cfg.dims)
+    ref = oracle.sketch_all_modes(X64, om)
+    Y = krp.krp_sketch_all_modes(xd, cfg.dims, [_dev(o) for o in om])
+    for n in range(4):
+        assert rel(Y[n].cpu().numpy(), ref[n]) <= Y_TOL
+    _, _, e_ref, _ = oracle.rhosvd(X64, om, ranks)
+    Q, core, e = krp.krp_rhosvd(xd, cfg.dims, ranks, [_dev(o) for o in om], with_error=True)
+    _check_factors(Q, ranks)
+    assert abs(e - e_ref) <= ERR_TOL, (e, e_ref)
+    oms = synth.sthosvd_omegas(cfg.dims, r, 0)
+    _, _, es_ref, _ = oracle.sthosvd(X64, oms, ranks)
+    _, _, es = krp.krp_sthosvd(xd, cfg.dims, ranks, [[None if o is None else _dev(o) for o in row] for row in oms],
+                               with_error=True)
+    assert abs(es - es_ref) <= ERR_TOL, (es, es_ref)

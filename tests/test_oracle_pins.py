@@ -465,3 +465,30 @@ def test_chunked_rhosvd_and_error_match_unchunked():
         assert np.allclose(np.abs(g1), np.abs(g0), rtol=1e-9, atol=1e-12)
         # the chunked error of the same decomposition equals the unchunked one
         assert abs(oracle.tucker_error(x, g0, q0, chunk=chunk) - e0) <= 1e-13
+
+
+def test_deterministic_hosvd_sthosvd_bounds():
+    """HOSVD / STHOSVD baselines (context for the Cauchy workload, NEXT-1): the textbook bounds
+    ||X - X̂||² <= Σ_n Σ_{j>r_n} σ_j²(X_(n)) (De Lathauwer et al. 2000; P:612 tail sums) and >= the largest
+    single-mode tail (Eckart–Young), exact recovery when the ranks cover the multilinear rank, and the
+    paper's observation that the randomized KRP variants come close to HOSVD on the Cauchy tensor."""
+    cfg = synth.config("cauchy").scaled((14, 12, 10, 9))
+    x = oracle.as_tensor(synth.tensor(cfg, 0), cfg.dims)
+    ranks = (4, 4, 4, 4)
+    tails = [float(np.sum(np.linalg.svd(oracle.unfold(x, n), compute_uv=False)[r:] ** 2)) for n, r in enumerate(ranks)]
+    nx2 = float(np.sum(x ** 2))
+    for fn in (oracle.hosvd, oracle.sthosvd_deterministic):
+        us, g, err = fn(x, ranks)
+        e2 = err ** 2 * nx2
+        assert e2 <= sum(tails) * (1 + 1e-9) and e2 >= max(tails) * (1 - 1e-9)
+        for u, r in zip(us, ranks):
+            assert np.allclose(u.T @ u, np.eye(r), atol=1e-12)
+    # exact recovery of a multilinear-rank-(2,2,2) tensor
+    g0 = _rng(77).standard_normal((2, 2, 2))
+    fac = [np.linalg.qr(_rng(78 + k).standard_normal((n, 2)))[0] for k, n in enumerate((7, 6, 5))]
+    xt = oracle.multi_ttm(g0, fac)
+    assert oracle.hosvd(xt, (2, 2, 2))[2] < 1e-12 and oracle.sthosvd_deterministic(xt, (2, 2, 2))[2] < 1e-12
+    # the memoized randomized variant with no oversampling is within a small factor of HOSVD (Fig. 2 setup)
+    om = synth.omegas(cfg.dims, 4, 3)
+    e_memo = oracle.rhosvd(x, om, ranks)[2]
+    assert oracle.hosvd(x, ranks)[2] <= e_memo <= 10 * oracle.hosvd(x, ranks)[2]
