@@ -69,7 +69,10 @@ enum {
   KRP_OP_RHOSVD = 2,
   KRP_OP_STHOSVD = 3,
   KRP_OP_SKETCH_ALL_HOST = 4, /* krp_sketch_all_modes_host: includes device copies of X, Omega, Y */
-  KRP_OP_RHOSVD_ERR = 5       /* krp_rhosvd with rel_err != NULL */
+  KRP_OP_RHOSVD_ERR = 5,      /* krp_rhosvd with rel_err != NULL */
+  KRP_OP_RHOSVD_FRESH = 6,    /* krp_rhosvd_fresh (rel_err buffers included) */
+  KRP_OP_RHOSVD_GAUSSIAN = 7, /* krp_rhosvd_gaussian (includes the explicit unfolding buffer) */
+  KRP_OP_STHOSVD_GAUSSIAN = 8 /* krp_sthosvd_gaussian */
 };
 
 KRP_API const char* krp_status_string(int status);
@@ -113,6 +116,25 @@ KRP_API int krp_rhosvd(const float* X, int d, const int64_t* dims, const int* ra
  * j == i are not read.  For j < i only the leading r_j rows are read (reading R5). */
 KRP_API int krp_sthosvd(const float* X, int d, const int64_t* dims, const int* ranks, int R, const float* const* omega,
                 float* const* Q, float* core, double* rel_err, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------ the paper's other variants (NEXT-2)
+ * RHOSVD-KRP, Alg. 7 read literally ("a fresh sequence ... each time"): mode n is sketched
+ * with its own sequence omega_steps[n*d + j] (I_j x R, j != n; layout as krp_sthosvd's omega), 2dNR sketch
+ * flops instead of the memoized 4NR; QR, core and truncation as krp_rhosvd. */
+KRP_API int krp_rhosvd_fresh(const float* X, int d, const int64_t* dims, const int* ranks, int R,
+                             const float* const* omega_steps, float* const* Q, float* core, double* rel_err, void* ws,
+                             size_t ws_bytes, void* stream);
+/* The dense-Gaussian baselines of Table 1: RHOSVD sketches mode n with omega_dense[n], a dense
+ * (N/I_n) x R row-major Gaussian whose rows follow the column order of X_(n); RSTHOSVD sketches step i's
+ * current core with omega_dense[i], (prod_{j<i} r_j * prod_{j>i} I_j) x R.  The unfolding is explicit (a
+ * batched transpose; the paper's "Unfolding" cost) and the product is an fp32 SGEMM (cuBLAS, loaded at run
+ * time; KRP_EUNSUPPORTED if it cannot be loaded).  Baselines for comparison, not the product's hot path. */
+KRP_API int krp_rhosvd_gaussian(const float* X, int d, const int64_t* dims, const int* ranks, int R,
+                                const float* const* omega_dense, float* const* Q, float* core, double* rel_err,
+                                void* ws, size_t ws_bytes, void* stream);
+KRP_API int krp_sthosvd_gaussian(const float* X, int d, const int64_t* dims, const int* ranks, int R,
+                                 const float* const* omega_dense, float* const* Q, float* core, double* rel_err,
+                                 void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------ multi-GPU (slab sharding)
  * The tensor is split into contiguous slabs along its LAST mode (contiguous in memory).  Each

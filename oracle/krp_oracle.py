@@ -50,6 +50,9 @@ __all__ = [
     "sketch_flops",
     "hosvd",
     "sthosvd_deterministic",
+    "rhosvd_fresh",
+    "rhosvd_gaussian",
+    "sthosvd_gaussian",
 ]
 
 
@@ -263,8 +266,14 @@ def rhosvd(x: np.ndarray, omegas: Sequence[np.ndarray], ranks: Sequence[int], ch
        then G <- G ×_1 U_1ᵀ ... ×_d U_dᵀ
     5. relative error ||X - [G; Q]|| / ||X||
     Returns (qs, core, err, ys)."""
+    return _rhosvd_from_sketches(x, sketch_all_modes(x, omegas, chunk), ranks, chunk, with_error)
+
+
+def _rhosvd_from_sketches(x: np.ndarray, ys: Sequence[np.ndarray], ranks: Sequence[int], chunk: Optional[int],
+                          with_error: bool):
+    """Alg. 7 lines 4-7 + truncation R4, given the d sketches Y_n."""
     d = x.ndim
-    ys = sketch_all_modes(x, omegas, chunk)
+    ys = list(ys)
     qs = [thin_qr(y)[0] for y in ys]
     g = _core_slabwise(x, qs, chunk)
     us = [None] * d
@@ -317,6 +326,44 @@ def sthosvd(x: np.ndarray, om_steps: Sequence[Sequence[Optional[np.ndarray]]], r
         qs.append(q)
     err = tucker_error(x, g, qs) if with_error else None
     return qs, g, err, ys
+
+
+# ----------------------------------------------------------------- NEXT-2: fresh-Ω KRP and dense-Gaussian variants
+def rhosvd_fresh(x: np.ndarray, om_steps: Sequence[Sequence[Optional[np.ndarray]]], ranks: Sequence[int],
+                 with_error: bool = True):
+    """RHOSVD-KRP, Alg. 7 read literally (P:522, P:529): for every mode n a fresh sequence {Omega^(n)_j}_{j != n}
+    (om_steps[n][j]) and Y_n = X_(n) (Omega^(n)_d ⊙ ... ⊙ Omega^(n)_1); then QR, core and truncation as in
+    ``rhosvd``.  2dNR sketch flops instead of 4NR."""
+    ys = [sketch_mode(x, om_steps[n], n) for n in range(x.ndim)]
+    return _rhosvd_from_sketches(x, ys, ranks, None, with_error)
+
+
+def rhosvd_gaussian(x: np.ndarray, om_dense: Sequence[np.ndarray], ranks: Sequence[int], with_error: bool = True):
+    """RHOSVD with dense Gaussian test matrices (the paper's baseline, Table 1): Y_n = X_(n) Omega_n with
+    Omega_n in R^{(N/I_n) x l} iid N(0,1), rows in the column order of X_(n)."""
+    ys = [unfold(x, n) @ np.asarray(om_dense[n], dtype=np.float64) for n in range(x.ndim)]
+    return _rhosvd_from_sketches(x, ys, ranks, None, with_error)
+
+
+def sthosvd_gaussian(x: np.ndarray, om_dense: Sequence[np.ndarray], ranks: Sequence[int], with_error: bool = True):
+    """RSTHOSVD with dense Gaussian test matrices (Table 1 baseline): step i sketches the current core,
+    Y_i = G_(i) Omega_i with Omega_i in R^{(N_i/I_i) x l} (N_i = the current core size), then the
+    Alg. 8 steps of ``sthosvd`` (QR, B = G ×_i Qᵀ, truncation by the SVD of B_(i))."""
+    g = x
+    qs = []
+    for i in range(x.ndim):
+        y = unfold(g, i) @ np.asarray(om_dense[i], dtype=np.float64)
+        q, _ = thin_qr(y)
+        b = ttm(g, q.T, i)
+        r = int(ranks[i])
+        if r < q.shape[1]:
+            u, _ = leading_left_singular_vectors(unfold(b, i), r)
+            q = q @ u
+            b = ttm(b, u.T, i)
+        g = b
+        qs.append(q)
+    err = tucker_error(x, g, qs) if with_error else None
+    return qs, g, err
 
 
 # ----------------------------------------------------------------- deterministic baselines (context for NEXT-1)

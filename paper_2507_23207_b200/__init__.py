@@ -23,12 +23,14 @@ __all__ = [
     "OP_RHOSVD_ERR", "krp_workspace_bytes",
     "krp_sketch_all_modes", "krp_sketch_all_modes_host", "krp_sketch_mode", "krp_rhosvd", "krp_sthosvd",
     "krp_launch_count", "krp_reset_launch_count", "Comm", "krp_sketch_all_modes_dist", "krp_rhosvd_dist",
-    "krp_sthosvd_dist",
+    "krp_sthosvd_dist", "krp_rhosvd_fresh", "krp_rhosvd_gaussian", "krp_sthosvd_gaussian", "OP_RHOSVD_FRESH",
+    "OP_RHOSVD_GAUSSIAN", "OP_STHOSVD_GAUSSIAN",
     "krp_workspace_bytes_dist", "EXPORTED_SYMBOLS", "LIB_PATH", "krp_slab_range", "krp_pack_layout",
 ]
 
 LIB_PATH = os.environ.get("KRP_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libkrp.so")
-OP_SKETCH_ALL, OP_SKETCH_MODE, OP_RHOSVD, OP_STHOSVD, OP_SKETCH_ALL_HOST, OP_RHOSVD_ERR = range(6)
+(OP_SKETCH_ALL, OP_SKETCH_MODE, OP_RHOSVD, OP_STHOSVD, OP_SKETCH_ALL_HOST, OP_RHOSVD_ERR, OP_RHOSVD_FRESH,
+ OP_RHOSVD_GAUSSIAN, OP_STHOSVD_GAUSSIAN) = range(9)
 
 # every function declared in include/krp.h
 EXPORTED_SYMBOLS = [
@@ -37,7 +39,7 @@ EXPORTED_SYMBOLS = [
     "krp_comm_id_bytes", "krp_comm_get_unique_id", "krp_comm_init", "krp_comm_destroy",
     "krp_sketch_all_modes_dist", "krp_rhosvd_dist", "krp_sthosvd_dist", "krp_workspace_bytes_dist", "krp_launch_count",
     "krp_reset_launch_count", "krp_profile_enable", "krp_profile_read", "krp_profile_reset",
-    "krp_slab_range", "krp_pack_layout",
+    "krp_slab_range", "krp_pack_layout", "krp_rhosvd_fresh", "krp_rhosvd_gaussian", "krp_sthosvd_gaussian",
 ]
 
 _lib = None
@@ -79,6 +81,9 @@ def lib() -> ctypes.CDLL:
         l_.krp_rhosvd.argtypes = [_P, ctypes.c_int, _I64P, _IP, ctypes.c_int, ptrs, ptrs, _P,
                                   ctypes.POINTER(ctypes.c_double), _P, ctypes.c_size_t, _P]
         l_.krp_sthosvd.argtypes = l_.krp_rhosvd.argtypes
+        l_.krp_rhosvd_fresh.argtypes = l_.krp_rhosvd.argtypes
+        l_.krp_rhosvd_gaussian.argtypes = l_.krp_rhosvd.argtypes
+        l_.krp_sthosvd_gaussian.argtypes = l_.krp_rhosvd.argtypes
         l_.krp_comm_id_bytes.restype = ctypes.c_size_t
         l_.krp_comm_get_unique_id.argtypes = [_P]
         l_.krp_comm_init.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, ctypes.c_int, _P]
@@ -354,3 +359,43 @@ def krp_sthosvd_dist(X_slab: torch.Tensor, dims_local: Sequence[int], I_d_global
                                   ctypes.byref(err) if with_error else None, w.data_ptr(), w.numel(), comm.handle,
                                   _stream(stream)), "krp_sthosvd_dist")
     return Q, core, (err.value if with_error else None)
+
+
+def _decomp(fname, op, X, dims, ranks, ptrs, R, with_error, ws, stream):
+    Q = [torch.empty((int(n), int(r)), dtype=torch.float32, device=X.device) for n, r in zip(dims, ranks)]
+    core = torch.empty(int(torch.tensor(list(ranks)).prod()), dtype=torch.float32, device=X.device)
+    err = ctypes.c_double(0.0)
+    w = _ws(krp_workspace_bytes(op, dims, R, ranks), X.device, ws)
+    _check(getattr(lib(), fname)(X.data_ptr(), len(dims), _dims(dims), _ints(ranks), R, _ptr_array(ptrs),
+                                 _ptr_array(Q), core.data_ptr(), ctypes.byref(err) if with_error else None,
+                                 w.data_ptr(), w.numel(), _stream(stream)), fname)
+    return Q, core, (err.value if with_error else None)
+
+
+def krp_rhosvd_fresh(X: torch.Tensor, dims: Sequence[int], ranks: Sequence[int],
+                     omega_steps: Sequence[Sequence[Optional[torch.Tensor]]], with_error: bool = False, ws=None,
+                     stream=None):
+    """RHOSVD-KRP, Alg. 7 literally: omega_steps[n][j] is mode n's fresh I_j x R factor (None for j == n)."""
+    _dev_f32(X, "X")
+    d = len(dims)
+    R = int(omega_steps[0][1].shape[1])
+    flat = [omega_steps[i][j] for i in range(d) for j in range(d)]
+    return _decomp("krp_rhosvd_fresh", OP_RHOSVD_FRESH, X, dims, ranks, flat, R, with_error, ws, stream)
+
+
+def krp_rhosvd_gaussian(X: torch.Tensor, dims: Sequence[int], ranks: Sequence[int],
+                        omega_dense: Sequence[torch.Tensor], with_error: bool = False, ws=None, stream=None):
+    """RHOSVD with dense Gaussian test matrices (Table 1 baseline): omega_dense[n] is (N/I_n) x R."""
+    _dev_f32(X, "X")
+    R = int(omega_dense[0].shape[1])
+    return _decomp("krp_rhosvd_gaussian", OP_RHOSVD_GAUSSIAN, X, dims, ranks, list(omega_dense), R, with_error, ws,
+                   stream)
+
+
+def krp_sthosvd_gaussian(X: torch.Tensor, dims: Sequence[int], ranks: Sequence[int],
+                         omega_dense: Sequence[torch.Tensor], with_error: bool = False, ws=None, stream=None):
+    """RSTHOSVD with dense Gaussian test matrices (Table 1 baseline): omega_dense[i] is (N_i/I_i) x R."""
+    _dev_f32(X, "X")
+    R = int(omega_dense[0].shape[1])
+    return _decomp("krp_sthosvd_gaussian", OP_STHOSVD_GAUSSIAN, X, dims, ranks, list(omega_dense), R, with_error, ws,
+                   stream)

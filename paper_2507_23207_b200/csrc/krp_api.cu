@@ -238,9 +238,19 @@ static int side_streams(SideStreams** out, std::unique_lock<std::mutex>& lk) {
 static int allreduce_sum_f32(DistCtx* c, float* buf, size_t count, cudaStream_t s);
 static int allreduce_sum_f64(DistCtx* c, double* buf, size_t count, cudaStream_t s);
 
+// Which sketch feeds the decomposition (NEXT-2): the memoized KRP sketch (one shared set), Alg. 7
+// read literally (a fresh KRP sequence per mode, steps[n*d + j]), or the dense-Gaussian baseline (Table 1:
+// dense[n] is (N/I_n) x R, or for STHOSVD the step's (N_i/I_i) x R).  Single-GPU only for the latter two.
+struct SketchVariant {
+  int kind = 0;  // 0 memoized KRP, 1 fresh KRP per mode, 2 dense Gaussian
+  const float* const* steps = nullptr;
+  const float* const* dense = nullptr;
+};
+
 static int rhosvd_impl(const float* X, const Dims& g /*local*/, int64_t Id_global, int64_t slab_begin,
                        const int* ranks, int R, const float* const* omega, float* const* Q, float* core,
-                       double* rel_err, Arena& ar, cudaStream_t s, DistCtx* dc, bool measure_only);
+                       double* rel_err, Arena& ar, cudaStream_t s, DistCtx* dc, bool measure_only,
+                       const SketchVariant* sv = nullptr);
 
 }  // namespace krp
 
@@ -322,8 +332,9 @@ namespace krp {
 
 static int rhosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_t slab_begin, const int* ranks, int R,
                        const float* const* omega, float* const* Q, float* core, double* rel_err, Arena& ar,
-                       cudaStream_t s, DistCtx* dc, bool measure_only) {
+                       cudaStream_t s, DistCtx* dc, bool measure_only, const SketchVariant* sv) {
   const int d = g.d;
+  const int kind = sv ? sv->kind : 0;
   const bool dist = dc != nullptr;
   int64_t gd[kMaxD];  // global dims
   for (int k = 0; k < d; ++k) gd[k] = g.n[k];
@@ -364,7 +375,12 @@ static int rhosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_t
   // scratch for the sketch / QR / gram / error (max of all)
   bool want[kMaxD];
   for (int k = 0; k < d; ++k) want[k] = true;
-  size_t scratch = sketch_ws_bytes(g, R, want);
+  size_t scratch = kind == 0 ? sketch_ws_bytes(g, R, want) : 0;
+  for (int k = 0; k < d && kind != 0; ++k) {  // per-mode sketches of the variants
+    bool w1[kMaxD] = {};
+    w1[k] = true;
+    scratch = std::max(scratch, kind == 1 ? sketch_ws_bytes(g, R, w1) : gaussian_sketch_ws_bytes(g, k));
+  }
   {  // the d CholeskyQR2 run concurrently: disjoint scratch per mode
     size_t qr = 0;
     for (int k = 0; k < d; ++k) qr += cholqr_ws_bytes(gd[k], R);
@@ -419,7 +435,24 @@ static int rhosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_t
     Yloc[d - 1] = Ybuf[d - 1] + slab_begin * R;
     KRP_CHECK_CUDA(cudaMemsetAsync(Ypack, 0, ysum * sizeof(float), s));
   }
-  KRP_TRY(sketch(X, g, om, R, want, Yloc, ar, s));
+  if (kind == 0) {
+    KRP_TRY(sketch(X, g, om, R, want, Yloc, ar, s));
+  } else {
+    for (int n = 0; n < d; ++n) {
+      if (kind == 1) {  // Alg. 7 line 3 with this mode's own fresh sequence
+        OmegaPtrs on{};
+        for (int j = 0; j < d; ++j) on.p[j] = (j == n) ? nullptr : sv->steps[n * d + j];
+        bool w1[kMaxD] = {};
+        w1[n] = true;
+        float* Y1[kMaxD] = {};
+        Y1[n] = Yloc[n];
+        KRP_TRY(sketch(X, g, on, R, w1, Y1, ar, s));
+      } else {  // the dense-Gaussian baseline (Table 1)
+        KRP_TRY(gaussian_sketch_mode(X, g, n, sv->dense[n], R, Yloc[n], ar, s));
+      }
+      ar.off = scratch_mark;
+    }
+  }
   ar.off = scratch_mark;
   // ---- multi-GPU: one all-reduce(sum) of the packed sketches (the zero-padded Y_d doubles as the gather)
   if (dist) KRP_TRY(allreduce_sum_f32(dc, Ypack, static_cast<size_t>(ysum), s));
@@ -537,7 +570,7 @@ static int rhosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_t
 // zero-padded all-reduce, contracts the sharded mode locally and all-reduces the (small) partial core.
 static int sthosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_t slab_begin, const int* ranks, int R,
                         const float* const* omega, float* const* Q, float* core, double* rel_err, Arena& ar,
-                        cudaStream_t s, DistCtx* dc, bool measure_only) {
+                        cudaStream_t s, DistCtx* dc, bool measure_only, const float* const* dense = nullptr) {
   const int d = g.d;
   const bool dist = dc != nullptr;
   int64_t gd[kMaxD];  // global dims
@@ -568,7 +601,7 @@ static int sthosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_
       const Dims cg = make_dims(d, cur);
       bool want[kMaxD] = {};
       want[i] = true;
-      scratch = std::max(scratch, sketch_ws_bytes(cg, R, want));
+      scratch = std::max(scratch, dense ? gaussian_sketch_ws_bytes(cg, i) : sketch_ws_bytes(cg, R, want));
       scratch = std::max(scratch, cholqr_ws_bytes(gd[i], R));
       cur[i] = R;
       scratch = std::max(scratch, mode_gram_ws_bytes(make_dims(d, cur), i));
@@ -625,7 +658,8 @@ static int sthosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_
     } else {
       Yp[i] = Y;
     }
-    KRP_TRY(sketch(G, cg, om, R, want, Yp, ar, s));
+    if (dense) KRP_TRY(gaussian_sketch_mode(G, cg, i, dense[i], R, Y, ar, s));  // the Table 1 baseline
+    else KRP_TRY(sketch(G, cg, om, R, want, Yp, ar, s));
     ar.off = mark;
     if (dist) KRP_TRY(allreduce_sum_f32(dc, Y, static_cast<size_t>(yrows * R), s));
     // 2. thin QR, replicated
@@ -787,10 +821,22 @@ static size_t ws_bytes_impl(int op, int d, const int64_t* dims, int64_t Id_globa
                   op == KRP_OP_RHOSVD_ERR ? &dummy : nullptr, ar, nullptr, nullptr, true);
       return ar.off + 256;
     }
-    case KRP_OP_STHOSVD: {
+    case KRP_OP_STHOSVD:
+    case KRP_OP_STHOSVD_GAUSSIAN: {
       if (!ranks) return 0;
       double dummy;
-      sthosvd_impl(nullptr, g, Id_global, 0, ranks, R, nullptr, nullptr, nullptr, &dummy, ar, nullptr, nullptr, true);
+      const float* const dummy_dense[kMaxD] = {};
+      sthosvd_impl(nullptr, g, Id_global, 0, ranks, R, nullptr, nullptr, nullptr, &dummy, ar, nullptr, nullptr, true,
+                   op == KRP_OP_STHOSVD_GAUSSIAN ? dummy_dense : nullptr);
+      return ar.off + 256;
+    }
+    case KRP_OP_RHOSVD_FRESH:
+    case KRP_OP_RHOSVD_GAUSSIAN: {
+      if (!ranks) return 0;
+      double dummy;
+      SketchVariant v;
+      v.kind = op == KRP_OP_RHOSVD_FRESH ? 1 : 2;
+      rhosvd_impl(nullptr, g, Id_global, 0, ranks, R, nullptr, nullptr, nullptr, &dummy, ar, nullptr, nullptr, true, &v);
       return ar.off + 256;
     }
     default:
@@ -928,6 +974,83 @@ int krp_sthosvd(const float* X, int d, const int64_t* dims, const int* ranks, in
   WsGuard guard;
   KRP_TRY(setup_arena(krp_workspace_bytes(KRP_OP_STHOSVD, d, dims, R, ranks), ws, ws_bytes, s, ar, guard));
   return sthosvd_impl(X, g, dims[d - 1], 0, ranks, R, omega, Q, core, rel_err, ar, s, nullptr, false);
+}
+
+static int validate_steps(const float* const* steps, int d, const char* what) {
+  if (!steps) {
+    set_error("%s is NULL", what);
+    return KRP_EINVAL;
+  }
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j)
+      if (i != j && !steps[i * d + j]) {
+        set_error("%s[%d*d+%d] is NULL", what, i, j);
+        return KRP_EINVAL;
+      }
+  return KRP_OK;
+}
+
+int krp_rhosvd_fresh(const float* X, int d, const int64_t* dims, const int* ranks, int R,
+                     const float* const* omega_steps, float* const* Q, float* core, double* rel_err, void* ws,
+                     size_t ws_bytes, void* stream) {
+  KRP_TRY(validate_common(X, d, dims, R));
+  KRP_TRY(validate_steps(omega_steps, d, "omega_steps"));
+  KRP_TRY(validate_ptrs(Q, d, -1, "Q"));
+  if (!core) {
+    set_error("core is NULL");
+    return KRP_EINVAL;
+  }
+  const Dims g = make_dims(d, dims);
+  KRP_TRY(validate_ranks(g, ranks, R));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Arena ar;
+  WsGuard guard;
+  KRP_TRY(setup_arena(krp_workspace_bytes(KRP_OP_RHOSVD_FRESH, d, dims, R, ranks), ws, ws_bytes, s, ar, guard));
+  SketchVariant v;
+  v.kind = 1;
+  v.steps = omega_steps;
+  return rhosvd_impl(X, g, dims[d - 1], 0, ranks, R, nullptr, Q, core, rel_err, ar, s, nullptr, false, &v);
+}
+
+int krp_rhosvd_gaussian(const float* X, int d, const int64_t* dims, const int* ranks, int R,
+                        const float* const* omega_dense, float* const* Q, float* core, double* rel_err, void* ws,
+                        size_t ws_bytes, void* stream) {
+  KRP_TRY(validate_common(X, d, dims, R));
+  KRP_TRY(validate_ptrs(omega_dense, d, -1, "omega_dense"));
+  KRP_TRY(validate_ptrs(Q, d, -1, "Q"));
+  if (!core) {
+    set_error("core is NULL");
+    return KRP_EINVAL;
+  }
+  const Dims g = make_dims(d, dims);
+  KRP_TRY(validate_ranks(g, ranks, R));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Arena ar;
+  WsGuard guard;
+  KRP_TRY(setup_arena(krp_workspace_bytes(KRP_OP_RHOSVD_GAUSSIAN, d, dims, R, ranks), ws, ws_bytes, s, ar, guard));
+  SketchVariant v;
+  v.kind = 2;
+  v.dense = omega_dense;
+  return rhosvd_impl(X, g, dims[d - 1], 0, ranks, R, nullptr, Q, core, rel_err, ar, s, nullptr, false, &v);
+}
+
+int krp_sthosvd_gaussian(const float* X, int d, const int64_t* dims, const int* ranks, int R,
+                         const float* const* omega_dense, float* const* Q, float* core, double* rel_err, void* ws,
+                         size_t ws_bytes, void* stream) {
+  KRP_TRY(validate_common(X, d, dims, R));
+  KRP_TRY(validate_ptrs(omega_dense, d, -1, "omega_dense"));
+  KRP_TRY(validate_ptrs(Q, d, -1, "Q"));
+  if (!core) {
+    set_error("core is NULL");
+    return KRP_EINVAL;
+  }
+  const Dims g = make_dims(d, dims);
+  KRP_TRY(validate_ranks(g, ranks, R));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Arena ar;
+  WsGuard guard;
+  KRP_TRY(setup_arena(krp_workspace_bytes(KRP_OP_STHOSVD_GAUSSIAN, d, dims, R, ranks), ws, ws_bytes, s, ar, guard));
+  return sthosvd_impl(X, g, dims[d - 1], 0, ranks, R, nullptr, Q, core, rel_err, ar, s, nullptr, false, omega_dense);
 }
 
 // ------------------------------------------------------------------ distributed

@@ -17,6 +17,12 @@ inline int sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, con
   return tc_sketch(X, g, om, R, want_mode, Y, ar, s);
 }
 
+// ---- the paper's dense-Gaussian baseline sketch (krp_baselines.cu): Y = X_(n) Omega_dense, Omega_dense
+// (N/I_n) x R row-major in the column order of X_(n); explicit unfolding + fp32 SGEMM (cuBLAS via dlopen)
+size_t gaussian_sketch_ws_bytes(const Dims& g, int n);
+int gaussian_sketch_mode(const float* X, const Dims& g, int n, const float* omega_dense, int R, float* Y, Arena& ar,
+                         cudaStream_t s);
+
 // ---- dense linear algebra (krp_linalg.cu)
 // CholeskyQR with shifted first pass and two refinement passes (sCholeskyQR3; plain CholeskyQR2
 // when the first Cholesky succeeds without shift).  Y: rows x R fp32 row-major.

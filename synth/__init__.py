@@ -45,6 +45,9 @@ __all__ = [
     "tucker_parts",
     "random_tensor",
     "cauchy_device",
+    "rhosvd_fresh_omegas",
+    "dense_gaussian",
+    "dense_gaussian_sthosvd",
 ]
 
 
@@ -112,6 +115,31 @@ def sthosvd_omegas(dims: Sequence[int], R: int, seed: int) -> List[List[Optional
     d = len(dims)
     return [[None if j == i else rng(seed, 300, i, j).standard_normal((int(dims[j]), R)).astype(np.float32)
              for j in range(d)] for i in range(d)]
+
+
+def rhosvd_fresh_omegas(dims: Sequence[int], R: int, seed: int) -> List[List[Optional[np.ndarray]]]:
+    """Alg. 7 read literally (NEXT-2): a fresh set per mode n, om[n][j] is I_j x R (j != n).
+    Tags (400, n, j)."""
+    d = len(dims)
+    return [[None if j == n else rng(seed, 400, n, j).standard_normal((int(dims[j]), R)).astype(np.float32)
+             for j in range(d)] for n in range(d)]
+
+
+def dense_gaussian(dims: Sequence[int], R: int, seed: int) -> List[np.ndarray]:
+    """Dense Gaussian test matrices of the RHOSVD baseline (Table 1): Omega_n is (N / I_n) x R, iid N(0,1),
+    fp32, row-major, rows in the column order of X_(n).  Tags (500, n)."""
+    N = int(np.prod(dims))
+    return [rng(seed, 500, n).standard_normal((N // int(dims[n]), R)).astype(np.float32) for n in range(len(dims))]
+
+
+def dense_gaussian_sthosvd(dims: Sequence[int], ranks: Sequence[int], R: int, seed: int) -> List[np.ndarray]:
+    """Dense Gaussian test matrices of the RSTHOSVD baseline: step i sketches the current core (modes j < i already
+    compressed to r_j), Omega_i is (prod_{j<i} r_j prod_{j>i} I_j) x R.  Tags (600, i)."""
+    out = []
+    for i in range(len(dims)):
+        rows = int(np.prod([ranks[j] for j in range(i)] + [dims[j] for j in range(i + 1, len(dims))]))
+        out.append(rng(seed, 600, i).standard_normal((rows, R)).astype(np.float32))
+    return out
 
 
 def _orth_factor(n: int, r: int, seed: int, k: int) -> np.ndarray:

@@ -287,3 +287,44 @@ def test_cauchy_workload_vs_oracle(krp, r):
     _, _, es = krp.krp_sthosvd(xd, cfg.dims, ranks, [[None if o is None else _dev(o) for o in row] for row in oms],
                                with_error=True)
     assert abs(es - es_ref) <= ERR_TOL, (es, es_ref)
+
+
+# ----------------------------------------------------------------- NEXT-2: fresh-Ω KRP and dense-Gaussian baselines
+@pytest.mark.parametrize("name,small", [("c2", (64, 48, 40)), ("c4", (16, 12, 10, 9, 8))])
+def test_rhosvd_fresh_and_gaussian_vs_oracle(krp, name, small):
+    """Alg. 7 read literally (a fresh KRP sequence per mode) and the dense-Gaussian RHOSVD / RSTHOSVD baselines
+    (Table 1) against the oracle on the same inputs."""
+    cfg = synth.config(name).scaled(small)
+    R = min(cfg.R, min(small))
+    ranks = tuple(min(r, R) for r in cfg.ranks)
+    x = synth.tensor(cfg, 0)
+    X64 = oracle.as_tensor(x, cfg.dims)
+    steps = synth.rhosvd_fresh_omegas(cfg.dims, R, 0)
+    _, _, e_ref, _ = oracle.rhosvd_fresh(X64, steps, ranks)
+    Q, core, e = krp.krp_rhosvd_fresh(_dev(x), cfg.dims, ranks, [[None if o is None else _dev(o) for o in row]
+                                                              for row in steps], with_error=True)
+    _check_factors(Q, ranks)
+    assert abs(e - e_ref) <= ERR_TOL, (e, e_ref)
+    dense = synth.dense_gaussian(cfg.dims, R, 0)
+    _, _, eg_ref, _ = oracle.rhosvd_gaussian(X64, dense, ranks)
+    _, _, eg = krp.krp_rhosvd_gaussian(_dev(x), cfg.dims, ranks, [_dev(o) for o in dense], with_error=True)
+    assert abs(eg - eg_ref) <= ERR_TOL, (eg, eg_ref)
+    dst = synth.dense_gaussian_sthosvd(cfg.dims, ranks, R, 0)
+    _, _, es_ref = oracle.sthosvd_gaussian(X64, dst, ranks)
+    _, _, es = krp.krp_sthosvd_gaussian(_dev(x), cfg.dims, ranks, [_dev(o) for o in dst], with_error=True)
+    assert abs(es - es_ref) <= ERR_TOL, (es, es_ref)
+
+
+def test_gaussian_sketch_with_kr_matrix_equals_krp_sketch(krp):
+    """A dense test matrix equal to the Khatri-Rao product makes the baseline's sketch the KRP sketch: pins the
+    explicit unfolding (column order of X_(n)) of the dense path on the device."""
+    dims, R = (24, 20, 18, 7), 6
+    x = synth.random_tensor(dims, 5, 4)
+    om = synth.omegas(dims, R, 5)
+    dense = [oracle.kr_for_mode(om, n).astype(np.float32) for n in range(4)]
+    ranks = (R,) * 4
+    Qg, cg, eg = krp.krp_rhosvd_gaussian(_dev(x), dims, ranks, [_dev(o) for o in dense], with_error=True)
+    Qk, ck, ek = krp.krp_rhosvd(_dev(x), dims, ranks, [_dev(o) for o in om], with_error=True)
+    assert abs(eg - ek) <= 1e-5 * max(1.0, ek), (eg, ek)
+    for a, b in zip(Qg, Qk):  # same sketches -> same Q up to the sketch's rounding
+        assert np.abs(np.abs(a.double().cpu().numpy().T @ b.double().cpu().numpy()) - np.eye(R)).max() < 1e-3

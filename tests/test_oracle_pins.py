@@ -492,3 +492,31 @@ def test_deterministic_hosvd_sthosvd_bounds():
     om = synth.omegas(cfg.dims, 4, 3)
     e_memo = oracle.rhosvd(x, om, ranks)[2]
     assert oracle.hosvd(x, ranks)[2] <= e_memo <= 10 * oracle.hosvd(x, ranks)[2]
+
+
+def test_fresh_and_gaussian_variants_reduce_to_memo():
+    """NEXT-2 pins.  (1) Alg. 7 with every mode's fresh sequence equal to the memoized set IS RHOSVD-KRP-MEMO
+    (P:571).  (2) A dense test matrix equal to the Khatri-Rao product turns the Gaussian sketch into the KRP
+    sketch, which pins the dense variant's unfolding / row order.  (3) Fresh sequences and
+    dense Gaussians both recover a noise-free Tucker tensor exactly (the randomized range finder)."""
+    cfg = synth.config("c2").scaled((12, 10, 9))
+    x = oracle.as_tensor(synth.tensor(cfg, 2), cfg.dims)
+    R, ranks = 6, (4, 4, 4)
+    om = synth.omegas(cfg.dims, R, 2)
+    q0, g0, e0, y0 = oracle.rhosvd(x, om, ranks)
+    same = [[None if j == n else om[j] for j in range(3)] for n in range(3)]
+    q1, g1, e1, y1 = oracle.rhosvd_fresh(x, same, ranks)
+    assert abs(e1 - e0) < 1e-13 and all(np.allclose(a, b, rtol=1e-13, atol=1e-13) for a, b in zip(y0, y1))
+    dense = [oracle.kr_for_mode(om, n) for n in range(3)]
+    q2, g2, e2, y2 = oracle.rhosvd(x, om, ranks)
+    _, _, e3, _ = oracle.rhosvd_gaussian(x, dense, ranks)
+    assert abs(e3 - e0) < 1e-12
+    for n in range(3):
+        assert np.allclose(oracle.unfold(x, n) @ dense[n], y0[n], rtol=1e-12, atol=1e-12)
+    # exact recovery with genuinely fresh / dense randomness
+    ct = synth.Config("t", (12, 10, 9), 6, (3, 3, 3), "tucker", core=(3, 3, 3))
+    core, us, _ = synth.tucker_parts(ct, 1)
+    xt = oracle.multi_ttm(core, us)  # fp64, exactly multilinear rank (3, 3, 3)
+    assert oracle.rhosvd_fresh(xt, synth.rhosvd_fresh_omegas(ct.dims, 6, 1), (3, 3, 3))[2] < 1e-12
+    assert oracle.rhosvd_gaussian(xt, synth.dense_gaussian(ct.dims, 6, 1), (3, 3, 3))[2] < 1e-12
+    assert oracle.sthosvd_gaussian(xt, synth.dense_gaussian_sthosvd(ct.dims, (3, 3, 3), 6, 1), (3, 3, 3))[2] < 1e-12
