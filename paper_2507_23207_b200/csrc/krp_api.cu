@@ -427,8 +427,11 @@ static int rhosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_t
 
   KRP_CHECK_CUDA(cudaMemsetAsync(flag, 0, kMaxD * sizeof(int), s));
   // ---- 1. memoized all-mode sketch of the local slab (Alg. 7 line 3 with memoization)
-  OmegaPtrs om = make_om(omega, d, -1);
-  if (dist) om.p[d - 1] = omega[d - 1] + slab_begin * R;  // local rows of the global Omega_d
+  OmegaPtrs om{};
+  if (kind == 0) {
+    om = make_om(omega, d, -1);
+    if (dist) om.p[d - 1] = omega[d - 1] + slab_begin * R;  // local rows of the global Omega_d
+  }
   float* Yloc[kMaxD];
   for (int k = 0; k < d; ++k) Yloc[k] = Ybuf[k];
   if (dist) {
@@ -646,8 +649,10 @@ static int sthosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_
     // 1. Y_i = G_(i) (⊙_{j != i} Omega^{(i)}_j), compressed modes read only their leading r_j rows; the
     //    sharded mode reads its slab rows
     OmegaPtrs om{};
-    for (int j = 0; j < d; ++j) om.p[j] = (j == i) ? nullptr : omega[i * d + j];
-    if (dist && !last) om.p[d - 1] = omega[i * d + d - 1] + slab_begin * R;
+    if (!dense) {
+      for (int j = 0; j < d; ++j) om.p[j] = (j == i) ? nullptr : omega[i * d + j];
+      if (dist && !last) om.p[d - 1] = omega[i * d + d - 1] + slab_begin * R;
+    }
     bool want[kMaxD] = {};
     want[i] = true;
     float* Yp[kMaxD] = {};
