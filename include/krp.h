@@ -136,6 +136,23 @@ KRP_API int krp_sthosvd_gaussian(const float* X, int d, const int64_t* dims, con
                                  const float* const* omega_dense, float* const* Q, float* core, double* rel_err,
                                  void* ws, size_t ws_bytes, void* stream);
 
+/* Randomized HOSVD of the Hadamard product of two 3-way Tucker tensors (App. C, Alg. 9):
+ * X = F x_1 A_1 x_2 A_2 x_3 A_3 (F: q_1 x q_2 x q_3, A_k: n_k x q_k), Y = G x_k U_k (G: s_1 x s_2 x s_3,
+ * U_k: n_k x s_k), all fp32 device arrays, cores first-index-fastest, factors row-major.  The product
+ * Z = X * Y (n_1 n_2 n_3 entries) is never formed: with H = F (x) G (the Kronecker core, q_k s_k per mode)
+ * and the row-wise Kronecker factors A_k (.)^T U_k, mode i's sketch Z_(i)(Omega_{i,k} (.) Omega_{i,j}) is
+ * (A_i (.)^T U_i) H_(i) (M_k (.) M_j) with M_j = (A_j^T (.) U_j^T) Omega_{i,j}; H_(i)(...) runs on
+ * the KRP sketch kernel.  omega[i*3 + j] (j != i): Omega_{i,j}, n_j x l_i.  ls[i] = l_i in [1, 64] (the sketch
+ * width r_i + oversampling), ranks[i] = r_i <= l_i; for r_i < l_i the HOSVD of the l-core truncates (reading
+ * R4; equal l_i are then required).  Outputs Q[i] (n_i x r_i, orthonormal) and core (r_1 r_2 r_3), with
+ * Z ~= core x_i Q_i.  Synchronizes the stream. */
+KRP_API size_t krp_hadamard_workspace_bytes(const int64_t* n, const int64_t* q, const int64_t* s, const int* ranks,
+                                            const int* ls);
+KRP_API int krp_hadamard_tucker(const float* F, const int64_t* q, const float* const* A, const float* G,
+                                const int64_t* s, const float* const* U, const int64_t* n, const int* ranks,
+                                const int* ls, const float* const* omega, float* const* Q, float* core, void* ws,
+                                size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------------ multi-GPU (slab sharding)
  * The tensor is split into contiguous slabs along its LAST mode (contiguous in memory).  Each
  * rank passes its local slab X (dims[d-1] = local slab length) plus the global last-mode size and

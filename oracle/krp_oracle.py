@@ -53,6 +53,9 @@ __all__ = [
     "rhosvd_fresh",
     "rhosvd_gaussian",
     "sthosvd_gaussian",
+    "row_kron",
+    "hadamard_tucker_explicit",
+    "hadamard_tucker_rhosvd",
 ]
 
 
@@ -364,6 +367,66 @@ def sthosvd_gaussian(x: np.ndarray, om_dense: Sequence[np.ndarray], ranks: Seque
         qs.append(q)
     err = tucker_error(x, g, qs) if with_error else None
     return qs, g, err
+
+
+# ----------------------------------------------------------------- NEXT-4: Hadamard products of Tucker tensors (App. C)
+def row_kron(a: np.ndarray, u: np.ndarray) -> np.ndarray:
+    """Transposed Khatri-Rao product A ⊙ᵀ U = (Aᵀ ⊙ Uᵀ)ᵀ, the row-wise Kronecker product: row i is
+    A(i,:) ⊗ U(i,:), column index a * s + alpha (U's index fastest)."""
+    a = np.asarray(a, dtype=np.float64)
+    u = np.asarray(u, dtype=np.float64)
+    return (a[:, :, None] * u[:, None, :]).reshape(a.shape[0], -1)
+
+
+def _tensor_kron(f: np.ndarray, g: np.ndarray) -> np.ndarray:
+    """F ⊗ G with H(A, B, C) = F(a,b,c) G(alpha,beta,gamma), A = alpha + a * q (P:960-962, 0-based)."""
+    h = np.multiply.outer(f, g)  # axes a, b, c, alpha, beta, gamma
+    d = f.ndim
+    perm = [x for k in range(d) for x in (k, d + k)]  # a, alpha, b, beta, c, gamma
+    h = np.transpose(h, perm)
+    return h.reshape([f.shape[k] * g.shape[k] for k in range(d)])
+
+
+def hadamard_tucker_explicit(f, xs, g, ys) -> np.ndarray:
+    """Z = X ∗ Y formed explicitly (small sizes only): X = F ×_n A_n, Y = G ×_n U_n."""
+    return multi_ttm(np.asarray(f, dtype=np.float64), list(xs)) * multi_ttm(np.asarray(g, dtype=np.float64), list(ys))
+
+
+def hadamard_tucker_rhosvd(f, xs, g, ys, ranks: Sequence[int], om: Sequence[Sequence[Optional[np.ndarray]]]):
+    """Alg. 9 (randomized HOSVD of the Hadamard product of two 3-way Tucker tensors), step by step:
+    1. Ω_{i,j} ∈ R^{n_j x l_i} (om[i][j], j != i; l_i = r_i + oversampling)
+    2. for each mode i: the sketch Z_(i)(⊙_{j != i, descending} Ω_{i,j}) computed through the structure
+       (P:989-993): M_j = (A_jᵀ ⊙ U_jᵀ) Ω_{i,j}  (q_j s_j x l_i), then
+       T = (F ⊗ G)_(i) (M_k ⊙ M_j)  (k > j the other two modes), then  Ẑ_i = (A_i ⊙ᵀ U_i) T
+       — the n_1 n_2 n_3 product Z is never formed;  Q_i = orth(Ẑ_i)
+    3. H = (F ⊗ G) ×_i Q_iᵀ(A_i ⊙ᵀ U_i)  (line 10, reading R23: its X, Y, Z are the orthonormal Q_i)
+    4. for r_i < l_i: truncation by the HOSVD of H (reading R4 applied to Alg. 9)
+    Returns (qs, core)."""
+    d = 3
+    f = np.asarray(f, dtype=np.float64)
+    g = np.asarray(g, dtype=np.float64)
+    fg = _tensor_kron(f, g)
+    qs = []
+    for i in range(d):
+        others = [j for j in range(d) if j != i]
+        ms = {j: row_kron(xs[j], ys[j]).T @ np.asarray(om[i][j], dtype=np.float64) for j in others}
+        # column-wise KR of the others in descending mode order (P:522): rows (j fastest, then k)
+        kr = khatri_rao(ms[others[1]], ms[others[0]])
+        t = unfold(fg, i) @ kr
+        zhat = row_kron(xs[i], ys[i]) @ t
+        qs.append(thin_qr(zhat)[0])
+    h = fg
+    for i in range(d):
+        h = ttm(h, qs[i].T @ row_kron(xs[i], ys[i]), i)
+    us = [None] * d
+    for i in range(d):
+        if int(ranks[i]) < qs[i].shape[1]:
+            us[i], _ = leading_left_singular_vectors(unfold(h, i), int(ranks[i]))
+    for i in range(d):
+        if us[i] is not None:
+            qs[i] = qs[i] @ us[i]
+            h = ttm(h, us[i].T, i)
+    return qs, h
 
 
 # ----------------------------------------------------------------- deterministic baselines (context for NEXT-1)

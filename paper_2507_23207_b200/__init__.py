@@ -13,6 +13,8 @@ from __future__ import annotations
 
 import ctypes
 import os
+
+import numpy as np
 from typing import List, Optional, Sequence, Tuple
 
 import torch
@@ -24,7 +26,7 @@ __all__ = [
     "krp_sketch_all_modes", "krp_sketch_all_modes_host", "krp_sketch_mode", "krp_rhosvd", "krp_sthosvd",
     "krp_launch_count", "krp_reset_launch_count", "Comm", "krp_sketch_all_modes_dist", "krp_rhosvd_dist",
     "krp_sthosvd_dist", "krp_rhosvd_fresh", "krp_rhosvd_gaussian", "krp_sthosvd_gaussian", "OP_RHOSVD_FRESH",
-    "OP_RHOSVD_GAUSSIAN", "OP_STHOSVD_GAUSSIAN",
+    "OP_RHOSVD_GAUSSIAN", "OP_STHOSVD_GAUSSIAN", "krp_hadamard_tucker",
     "krp_workspace_bytes_dist", "EXPORTED_SYMBOLS", "LIB_PATH", "krp_slab_range", "krp_pack_layout",
 ]
 
@@ -40,6 +42,7 @@ EXPORTED_SYMBOLS = [
     "krp_sketch_all_modes_dist", "krp_rhosvd_dist", "krp_sthosvd_dist", "krp_workspace_bytes_dist", "krp_launch_count",
     "krp_reset_launch_count", "krp_profile_enable", "krp_profile_read", "krp_profile_reset",
     "krp_slab_range", "krp_pack_layout", "krp_rhosvd_fresh", "krp_rhosvd_gaussian", "krp_sthosvd_gaussian",
+    "krp_hadamard_workspace_bytes", "krp_hadamard_tucker",
 ]
 
 _lib = None
@@ -82,6 +85,10 @@ def lib() -> ctypes.CDLL:
                                   ctypes.POINTER(ctypes.c_double), _P, ctypes.c_size_t, _P]
         l_.krp_sthosvd.argtypes = l_.krp_rhosvd.argtypes
         l_.krp_rhosvd_fresh.argtypes = l_.krp_rhosvd.argtypes
+        l_.krp_hadamard_workspace_bytes.restype = ctypes.c_size_t
+        l_.krp_hadamard_workspace_bytes.argtypes = [_I64P, _I64P, _I64P, _IP, _IP]
+        l_.krp_hadamard_tucker.argtypes = [_P, _I64P, ptrs, _P, _I64P, ptrs, _I64P, _IP, _IP, ptrs, ptrs, _P, _P,
+                                           ctypes.c_size_t, _P]
         l_.krp_rhosvd_gaussian.argtypes = l_.krp_rhosvd.argtypes
         l_.krp_sthosvd_gaussian.argtypes = l_.krp_rhosvd.argtypes
         l_.krp_comm_id_bytes.restype = ctypes.c_size_t
@@ -399,3 +406,25 @@ def krp_sthosvd_gaussian(X: torch.Tensor, dims: Sequence[int], ranks: Sequence[i
     R = int(omega_dense[0].shape[1])
     return _decomp("krp_sthosvd_gaussian", OP_STHOSVD_GAUSSIAN, X, dims, ranks, list(omega_dense), R, with_error, ws,
                    stream)
+
+
+def krp_hadamard_tucker(F: torch.Tensor, A: Sequence[torch.Tensor], G: torch.Tensor, U: Sequence[torch.Tensor],
+                        ranks: Sequence[int], omegas: Sequence[Sequence[Optional[torch.Tensor]]], ws=None, stream=None):
+    """Alg. 9: Tucker recompression of (F x_k A_k) * (G x_k U_k) without forming the product.  F, G are flat
+    first-index-fastest cores with shapes given by the factors; omegas[i][j] is n_j x l_i (None for j == i).
+    Returns (Q list, core)."""
+    n = [int(a.shape[0]) for a in A]
+    q = [int(a.shape[1]) for a in A]
+    s = [int(u.shape[1]) for u in U]
+    ls = [int(omegas[i][(i + 1) % 3].shape[1]) for i in range(3)]
+    for t in [F, G, *A, *U]:
+        _dev_f32(t, "argument")
+    Q = [torch.empty((n[i], int(ranks[i])), dtype=torch.float32, device=F.device) for i in range(3)]
+    core = torch.empty(int(np.prod(ranks)), dtype=torch.float32, device=F.device)
+    nb = int(lib().krp_hadamard_workspace_bytes(_dims(n), _dims(q), _dims(s), _ints(ranks), _ints(ls)))
+    w = _ws(nb, F.device, ws)
+    flat = [omegas[i][j] for i in range(3) for j in range(3)]
+    _check(lib().krp_hadamard_tucker(F.data_ptr(), _dims(q), _ptr_array(A), G.data_ptr(), _dims(s), _ptr_array(U),
+                                     _dims(n), _ints(ranks), _ints(ls), _ptr_array(flat), _ptr_array(Q),
+                                     core.data_ptr(), w.data_ptr(), w.numel(), _stream(stream)), "krp_hadamard_tucker")
+    return Q, core

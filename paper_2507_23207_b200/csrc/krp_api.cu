@@ -1058,6 +1058,55 @@ int krp_sthosvd_gaussian(const float* X, int d, const int64_t* dims, const int* 
   return sthosvd_impl(X, g, dims[d - 1], 0, ranks, R, nullptr, Q, core, rel_err, ar, s, nullptr, false, omega_dense);
 }
 
+static int validate_hadamard(const int64_t* n, const int64_t* q, const int64_t* s, const int* ranks, const int* ls) {
+  if (!n || !q || !s || !ranks || !ls) {
+    set_error("null size argument");
+    return KRP_EINVAL;
+  }
+  for (int k = 0; k < 3; ++k) {
+    if (n[k] < 1 || q[k] < 1 || s[k] < 1 || q[k] > n[k] || s[k] > n[k]) {
+      set_error("mode %d: n=%lld q=%lld s=%lld (need 1 <= q, s <= n)", k, static_cast<long long>(n[k]),
+                static_cast<long long>(q[k]), static_cast<long long>(s[k]));
+      return KRP_EINVAL;
+    }
+    if (ls[k] < 1 || ls[k] > kMaxRDecomp || ranks[k] < 1 || ranks[k] > ls[k] || ls[k] > n[k]) {
+      set_error("mode %d: l=%d, r=%d (need 1 <= r <= l <= min(n, %d))", k, ls[k], ranks[k], kMaxRDecomp);
+      return KRP_ESHAPE;
+    }
+  }
+  return KRP_OK;
+}
+
+size_t krp_hadamard_workspace_bytes(const int64_t* n, const int64_t* q, const int64_t* s, const int* ranks,
+                                    const int* ls) {
+  if (validate_hadamard(n, q, s, ranks, ls) != KRP_OK) return 0;
+  Arena ar;
+  ar.measuring = true;
+  hadamard_tucker_impl(nullptr, q, nullptr, nullptr, s, nullptr, n, ranks, ls, nullptr, nullptr, nullptr, ar, nullptr,
+                       true);
+  return ar.off + 256;
+}
+
+int krp_hadamard_tucker(const float* F, const int64_t* q, const float* const* A, const float* G, const int64_t* s,
+                        const float* const* U, const int64_t* n, const int* ranks, const int* ls,
+                        const float* const* omega, float* const* Q, float* core, void* ws, size_t ws_bytes,
+                        void* stream) {
+  KRP_TRY(validate_hadamard(n, q, s, ranks, ls));
+  if (!F || !G || !core) {
+    set_error("F, G or core is NULL");
+    return KRP_EINVAL;
+  }
+  KRP_TRY(validate_ptrs(A, 3, -1, "A"));
+  KRP_TRY(validate_ptrs(U, 3, -1, "U"));
+  KRP_TRY(validate_ptrs(Q, 3, -1, "Q"));
+  KRP_TRY(validate_steps(omega, 3, "omega"));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Arena ar;
+  WsGuard guard;
+  KRP_TRY(setup_arena(krp_hadamard_workspace_bytes(n, q, s, ranks, ls), ws, ws_bytes, st, ar, guard));
+  return hadamard_tucker_impl(F, q, A, G, s, U, n, ranks, ls, omega, Q, core, ar, st, false);
+}
+
 // ------------------------------------------------------------------ distributed
 size_t krp_comm_id_bytes(void) { return sizeof(krp::nccl_uid_t); }
 

@@ -23,6 +23,12 @@ size_t gaussian_sketch_ws_bytes(const Dims& g, int n);
 int gaussian_sketch_mode(const float* X, const Dims& g, int n, const float* omega_dense, int R, float* Y, Arena& ar,
                          cudaStream_t s);
 
+// ---- NEXT-4: randomized HOSVD of the Hadamard product of two 3-way Tucker tensors (krp_hadamard.cu, Alg. 9)
+int hadamard_tucker_impl(const float* F, const int64_t* q, const float* const* A, const float* G, const int64_t* s,
+                         const float* const* U, const int64_t* n, const int* ranks, const int* ls,
+                         const float* const* omega, float* const* Qout, float* core, Arena& ar, cudaStream_t st,
+                         bool measure_only);
+
 // ---- dense linear algebra (krp_linalg.cu)
 // CholeskyQR with shifted first pass and two refinement passes (sCholeskyQR3; plain CholeskyQR2
 // when the first Cholesky succeeds without shift).  Y: rows x R fp32 row-major.

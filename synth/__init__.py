@@ -48,6 +48,8 @@ __all__ = [
     "rhosvd_fresh_omegas",
     "dense_gaussian",
     "dense_gaussian_sthosvd",
+    "hadamard_tucker_inputs",
+    "hadamard_omegas",
 ]
 
 
@@ -140,6 +142,23 @@ def dense_gaussian_sthosvd(dims: Sequence[int], ranks: Sequence[int], R: int, se
         rows = int(np.prod([ranks[j] for j in range(i)] + [dims[j] for j in range(i + 1, len(dims))]))
         out.append(rng(seed, 600, i).standard_normal((rows, R)).astype(np.float32))
     return out
+
+
+def hadamard_tucker_inputs(ns: Sequence[int], qs: Sequence[int], ss: Sequence[int], seed: int):
+    """Two 3-way Tucker tensors X = F ×_n A_n (cores q) and Y = G ×_n U_n (cores s) with iid N(0,1) cores and
+    orthonormalised Gaussian factors (the App. C setting), fp32.  Tags (700, ...)."""
+    f = rng(seed, 700).standard_normal(tuple(qs)).astype(np.float32)
+    g = rng(seed, 701).standard_normal(tuple(ss)).astype(np.float32)
+    xs = [np.linalg.qr(rng(seed, 702, k).standard_normal((n, q)))[0].astype(np.float32) for k, (n, q) in enumerate(zip(ns, qs))]
+    ys = [np.linalg.qr(rng(seed, 703, k).standard_normal((n, q)))[0].astype(np.float32) for k, (n, q) in enumerate(zip(ns, ss))]
+    return f, xs, g, ys
+
+
+def hadamard_omegas(ns: Sequence[int], ls: Sequence[int], seed: int) -> List[List[Optional[np.ndarray]]]:
+    """Ω_{i,j} ∈ R^{n_j x l_i} (Alg. 9 line 2), iid N(0,1), fp32; None on the diagonal.  Tags (710, i, j)."""
+    d = len(ns)
+    return [[None if j == i else rng(seed, 710, i, j).standard_normal((int(ns[j]), int(ls[i]))).astype(np.float32)
+             for j in range(d)] for i in range(d)]
 
 
 def _orth_factor(n: int, r: int, seed: int, k: int) -> np.ndarray:

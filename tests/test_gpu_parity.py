@@ -328,3 +328,27 @@ def test_gaussian_sketch_with_kr_matrix_equals_krp_sketch(krp):
     assert abs(eg - ek) <= 1e-5 * max(1.0, ek), (eg, ek)
     for a, b in zip(Qg, Qk):  # same sketches -> same Q up to the sketch's rounding
         assert np.abs(np.abs(a.double().cpu().numpy().T @ b.double().cpu().numpy()) - np.eye(R)).max() < 1e-3
+
+
+# ----------------------------------------------------------------- NEXT-4: Hadamard product of Tucker tensors (Alg. 9)
+def test_hadamard_tucker_vs_oracle(krp):
+    """Alg. 9 on the device (the product Z = X ∗ Y is never formed) against the oracle's Alg. 9: the same
+    approximation error of Z (evaluated in fp64 on the explicit Z), orthonormal factors; and exact recovery
+    when every sketch width covers the product's multilinear rank q_n s_n."""
+    ns, qs_, ss = (60, 50, 40), (3, 4, 2), (2, 3, 4)
+    f, xs, g, ys = synth.hadamard_tucker_inputs(ns, qs_, ss, 5)
+    z = oracle.hadamard_tucker_explicit(f, xs, g, ys)
+    flat = lambda a: _dev(np.asarray(a).reshape(-1, order="F"))
+    for ls, ranks in [((8, 8, 8), (6, 6, 6)), ((6, 12, 8), (6, 12, 8))]:
+        om = synth.hadamard_omegas(ns, ls, 6)
+        qo, ho = oracle.hadamard_tucker_rhosvd(f, xs, g, ys, ranks, om)
+        e_ref = oracle.tucker_error(z, ho, qo)
+        Q, core = krp.krp_hadamard_tucker(flat(f), [_dev(a) for a in xs], flat(g), [_dev(u) for u in ys], ranks,
+                                          [[None if o is None else _dev(o) for o in row] for row in om])
+        _check_factors(Q, ranks)
+        qs = [q.double().cpu().numpy() for q in Q]
+        h = core.double().cpu().numpy().reshape(ranks, order="F")
+        e = oracle.tucker_error(z, h, qs)
+        assert abs(e - e_ref) <= ERR_TOL, (ls, e, e_ref)
+        if ls == ranks:
+            assert e < 1e-5, e

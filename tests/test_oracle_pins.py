@@ -520,3 +520,34 @@ def test_fresh_and_gaussian_variants_reduce_to_memo():
     assert oracle.rhosvd_fresh(xt, synth.rhosvd_fresh_omegas(ct.dims, 6, 1), (3, 3, 3))[2] < 1e-12
     assert oracle.rhosvd_gaussian(xt, synth.dense_gaussian(ct.dims, 6, 1), (3, 3, 3))[2] < 1e-12
     assert oracle.sthosvd_gaussian(xt, synth.dense_gaussian_sthosvd(ct.dims, (3, 3, 3), 6, 1), (3, 3, 3))[2] < 1e-12
+
+
+def test_hadamard_tucker_structured_equals_explicit():
+    """NEXT-4 pins (App. C): (1) the Hadamard product identity X ∗ Y = (F⊗G) ×_n (A_n ⊙ᵀ U_n) (eq. (C.1),
+    Kressner–Periša Lemma 3.1) holds elementwise; (2) Alg. 9's structured sketch equals the explicit MTTKRP of Z
+    with the same Ω (the derivation at P:989-993); (3) its core equals Z ×_n Q_nᵀ, so Ẑ is the orthogonal
+    projection of Z; (4) with l_i >= q_i s_i (the multilinear rank of Z) the recompression is exact."""
+    ns, qs_, ss = (9, 8, 7), (2, 3, 2), (3, 2, 3)
+    f, xs, g, ys = synth.hadamard_tucker_inputs(ns, qs_, ss, 3)
+    z = oracle.hadamard_tucker_explicit(f, xs, g, ys)
+    # (1) elementwise identity through the row-wise Kronecker factors
+    z2 = oracle.multi_ttm(_tk(f, g), [oracle.row_kron(a, u) for a, u in zip(xs, ys)])
+    assert np.allclose(z, z2, rtol=1e-12, atol=1e-13)
+    ls = (5, 4, 6)
+    om = synth.hadamard_omegas(ns, ls, 3)
+    qs, h = oracle.hadamard_tucker_rhosvd(f, xs, g, ys, ls, om)
+    for i in range(3):
+        omi = [np.ones((1, ls[i])) if j == i else om[i][j] for j in range(3)]
+        y = oracle.sketch_mode(z, omi, i)
+        q, _ = oracle.thin_qr(y)
+        assert np.allclose(np.abs(q.T @ qs[i]), np.eye(ls[i]), atol=1e-8)  # same range, same Q up to signs
+    assert np.allclose(h, oracle.multi_ttm(z, [q.T for q in qs]), rtol=1e-10, atol=1e-12)
+    # (4) exact when every l_i covers q_i s_i
+    lx = tuple(q * s for q, s in zip(qs_, ss))
+    qx, hx = oracle.hadamard_tucker_rhosvd(f, xs, g, ys, lx, synth.hadamard_omegas(ns, lx, 4))
+    assert oracle.tucker_error(z, hx, qx) < 1e-12
+
+
+def _tk(f, g):
+    from oracle.krp_oracle import _tensor_kron
+    return _tensor_kron(np.asarray(f, dtype=np.float64), np.asarray(g, dtype=np.float64))
