@@ -72,7 +72,8 @@ enum {
   KRP_OP_RHOSVD_ERR = 5,      /* krp_rhosvd with rel_err != NULL */
   KRP_OP_RHOSVD_FRESH = 6,    /* krp_rhosvd_fresh (rel_err buffers included) */
   KRP_OP_RHOSVD_GAUSSIAN = 7, /* krp_rhosvd_gaussian (includes the explicit unfolding buffer) */
-  KRP_OP_STHOSVD_GAUSSIAN = 8 /* krp_sthosvd_gaussian */
+  KRP_OP_STHOSVD_GAUSSIAN = 8, /* krp_sthosvd_gaussian */
+  KRP_OP_TTM = 9               /* krp_ttm: pass J as R (only mode n = 0 takes workspace) */
 };
 
 KRP_API const char* krp_status_string(int status);
@@ -97,6 +98,16 @@ KRP_API int krp_sketch_all_modes_host(const float* X_host, int d, const int64_t*
  * n is 0-based; omega[n] is not read (may be NULL).  2*N*R flops. */
 KRP_API int krp_sketch_mode(const float* X, int d, const int64_t* dims, int n, const float* const* omega, int R, float* Y,
                     void* ws, size_t ws_bytes, void* stream);
+
+/* Mode-n product Y = X x_n A (the core contractions G = X x_1 Q_1^T ... of Alg. 7 line 5, and
+ * B = G x_i Q^T of Alg. 8 line 5; definition of x_n as in S:124-128): A is J x I_n row-major
+ * (device), Y has dims with I_n replaced by J (device, first index fastest, written, not accumulated).
+ * Mode n = 0 with J <= 64, I_1 % 4 == 0 and X 16-byte aligned runs on the tensor cores (tcgen05,
+ * 3xTF32: fp32-level accuracy, fixed summation order); other shapes on fp32 FMA kernels.  ws: at least
+ * krp_workspace_bytes(KRP_OP_TTM, d, dims, J, NULL) bytes, or NULL (allocated and freed on the stream).
+ * Errors: KRP_EINVAL (null pointers, n out of range, J < 1), KRP_ENOMEM (ws too small). */
+KRP_API int krp_ttm(const float* X, int d, const int64_t* dims, int n, const float* A, int J, float* Y, void* ws,
+                    size_t ws_bytes, void* stream);
 
 /* RHOSVD-KRP-MEMO (Alg. 7 with memoization):
  *   Y_n = memoized sketch; Q_n = CholeskyQR2(Y_n) (thin QR with diag(R) > 0);

@@ -26,13 +26,13 @@ __all__ = [
     "krp_sketch_all_modes", "krp_sketch_all_modes_host", "krp_sketch_mode", "krp_rhosvd", "krp_sthosvd",
     "krp_launch_count", "krp_reset_launch_count", "Comm", "krp_sketch_all_modes_dist", "krp_rhosvd_dist",
     "krp_sthosvd_dist", "krp_rhosvd_fresh", "krp_rhosvd_gaussian", "krp_sthosvd_gaussian", "OP_RHOSVD_FRESH",
-    "OP_RHOSVD_GAUSSIAN", "OP_STHOSVD_GAUSSIAN", "krp_hadamard_tucker",
+    "OP_RHOSVD_GAUSSIAN", "OP_STHOSVD_GAUSSIAN", "krp_hadamard_tucker", "krp_ttm", "OP_TTM",
     "krp_workspace_bytes_dist", "EXPORTED_SYMBOLS", "LIB_PATH", "krp_slab_range", "krp_pack_layout",
 ]
 
 LIB_PATH = os.environ.get("KRP_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libkrp.so")
 (OP_SKETCH_ALL, OP_SKETCH_MODE, OP_RHOSVD, OP_STHOSVD, OP_SKETCH_ALL_HOST, OP_RHOSVD_ERR, OP_RHOSVD_FRESH,
- OP_RHOSVD_GAUSSIAN, OP_STHOSVD_GAUSSIAN) = range(9)
+ OP_RHOSVD_GAUSSIAN, OP_STHOSVD_GAUSSIAN, OP_TTM) = range(10)
 
 # every function declared in include/krp.h
 EXPORTED_SYMBOLS = [
@@ -42,7 +42,7 @@ EXPORTED_SYMBOLS = [
     "krp_sketch_all_modes_dist", "krp_rhosvd_dist", "krp_sthosvd_dist", "krp_workspace_bytes_dist", "krp_launch_count",
     "krp_reset_launch_count", "krp_profile_enable", "krp_profile_read", "krp_profile_reset",
     "krp_slab_range", "krp_pack_layout", "krp_rhosvd_fresh", "krp_rhosvd_gaussian", "krp_sthosvd_gaussian",
-    "krp_hadamard_workspace_bytes", "krp_hadamard_tucker",
+    "krp_hadamard_workspace_bytes", "krp_hadamard_tucker", "krp_ttm",
 ]
 
 _lib = None
@@ -81,6 +81,7 @@ def lib() -> ctypes.CDLL:
         l_.krp_sketch_all_modes_host.argtypes = l_.krp_sketch_all_modes.argtypes
         l_.krp_sketch_mode.argtypes = [_P, ctypes.c_int, _I64P, ctypes.c_int, ptrs, ctypes.c_int, _P, _P,
                                        ctypes.c_size_t, _P]
+        l_.krp_ttm.argtypes = [_P, ctypes.c_int, _I64P, ctypes.c_int, _P, ctypes.c_int, _P, _P, ctypes.c_size_t, _P]
         l_.krp_rhosvd.argtypes = [_P, ctypes.c_int, _I64P, _IP, ctypes.c_int, ptrs, ptrs, _P,
                                   ctypes.POINTER(ctypes.c_double), _P, ctypes.c_size_t, _P]
         l_.krp_sthosvd.argtypes = l_.krp_rhosvd.argtypes
@@ -224,6 +225,20 @@ def krp_sketch_mode(X: torch.Tensor, dims: Sequence[int], n: int, omegas: Sequen
     w = _ws(krp_workspace_bytes(OP_SKETCH_MODE, dims, R), X.device, ws)
     _check(lib().krp_sketch_mode(X.data_ptr(), len(dims), _dims(dims), int(n), _ptr_array(omegas), R, Y.data_ptr(),
                                  w.data_ptr(), w.numel(), _stream(stream)), "krp_sketch_mode")
+    return Y
+
+
+def krp_ttm(X: torch.Tensor, dims: Sequence[int], n: int, A: torch.Tensor, Y: Optional[torch.Tensor] = None,
+            ws: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """Y = X x_n A; A: J x I_n fp32 row-major on the device; Y flat, dims with I_n -> J."""
+    _dev_f32(X, "X")
+    _dev_f32(A, "A")
+    J = int(A.shape[0])
+    if Y is None:
+        Y = torch.empty(X.numel() // int(dims[n]) * J, dtype=torch.float32, device=X.device)
+    w = _ws(krp_workspace_bytes(OP_TTM, dims, J), X.device, ws)
+    _check(lib().krp_ttm(X.data_ptr(), len(dims), _dims(dims), int(n), A.data_ptr(), J, Y.data_ptr(), w.data_ptr(),
+                         w.numel(), _stream(stream)), "krp_ttm")
     return Y
 
 

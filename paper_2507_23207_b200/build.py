@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libkrp.so")
-SOURCES = ["krp_api.cu", "krp_sketch_tc.cu", "krp_linalg.cu", "krp_baselines.cu", "krp_hadamard.cu"]
+SOURCES = ["krp_api.cu", "krp_sketch_tc.cu", "krp_linalg.cu", "krp_baselines.cu", "krp_hadamard.cu", "krp_ttm_tc.cu"]
 HEADERS = ["krp_common.cuh", "krp_internal.h", "sm100.cuh", os.path.join("..", "..", "include", "krp.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo",

@@ -175,7 +175,7 @@ struct TtmOp {
   int64_t sj, si;
 };
 static int ttm_chain(const float* X, Dims g, const TtmOp* ops, float* bufA, float* bufB, float* out,
-                     cudaStream_t s) {
+                     cudaStream_t s, Arena* ar = nullptr) {
   const float* src = X;
   int last = -1;
   for (int k = 0; k < g.d; ++k)
@@ -188,7 +188,7 @@ static int ttm_chain(const float* X, Dims g, const TtmOp* ops, float* bufA, floa
   for (int k = 0; k < g.d; ++k) {
     if (!ops[k].A) continue;
     float* dst = (k == last) ? out : (use_a ? bufA : bufB);
-    KRP_TRY(ttm(src, g, k, ops[k].A, ops[k].J, ops[k].sj, ops[k].si, dst, s));
+    KRP_TRY(ttm(src, g, k, ops[k].A, ops[k].J, ops[k].sj, ops[k].si, dst, s, ar));
     int64_t nd[kMaxD];
     for (int m = 0; m < g.d; ++m) nd[m] = g.n[m];
     nd[k] = ops[k].J;
@@ -392,6 +392,7 @@ static int rhosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_t
     Dims cg = make_dims(d, cd);
     for (int k = 0; k < d; ++k) scratch = std::max(scratch, mode_gram_ws_bytes(cg, k));
   }
+  scratch = std::max(scratch, ttm_ws_bytes(g, 0, R));  // the first core contraction on the tensor cores
   // error pass buffers: slab chunks of the last mode
   const int64_t inner = g.N / g.n[d - 1];
   int64_t chunk = std::max<int64_t>(1, (int64_t(1) << 25) / std::max<int64_t>(inner, 1));
@@ -481,7 +482,7 @@ static int rhosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_t
   TtmOp ops[kMaxD];
   for (int k = 0; k < d; ++k) ops[k] = TtmOp{Qfull[k], R, 1, R};  // A = Q^T: (j,i) at Q[i*R + j]
   if (dist) ops[d - 1].A = Qfull[d - 1] + slab_begin * R;
-  KRP_TRY(ttm_chain(X, g, ops, CA, CB, G0, s));
+  KRP_TRY(ttm_chain(X, g, ops, CA, CB, G0, s, &ar));
   if (dist) KRP_TRY(allreduce_sum_f32(dc, G0, static_cast<size_t>(coreR), s));
   // ---- 4. truncation R -> r_n by HOSVD of the small core (reading R4): every U_n comes from the
   //      untruncated core G0, so the d Gram matrices and eigenproblems are independent (one batched
@@ -606,6 +607,7 @@ static int sthosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_
       want[i] = true;
       scratch = std::max(scratch, dense ? gaussian_sketch_ws_bytes(cg, i) : sketch_ws_bytes(cg, R, want));
       scratch = std::max(scratch, cholqr_ws_bytes(gd[i], R));
+      scratch = std::max(scratch, ttm_ws_bytes(cg, i, R));
       cur[i] = R;
       scratch = std::max(scratch, mode_gram_ws_bytes(make_dims(d, cur), i));
       cur[i] = ranks[i];
@@ -672,7 +674,8 @@ static int sthosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_
     ar.off = mark;
     // 3. B = G x_i Q^T: local; on the sharded mode the slab rows of Q, and the partial B is summed
     const float* Qrows = (dist && last) ? Qf + slab_begin * R : Qf;
-    KRP_TRY(ttm(G, cg, i, Qrows, R, 1, R, B, s));
+    KRP_TRY(ttm(G, cg, i, Qrows, R, 1, R, B, s, &ar));
+    ar.off = mark;
     int64_t bd[kMaxD];
     for (int k = 0; k < d; ++k) bd[k] = cur[k];
     bd[i] = R;
@@ -790,6 +793,11 @@ int krp_profile_read(double* kernel_ms, uint64_t* launches, double* alg_bytes, d
 void krp_reset_launch_count(void) { krp::g_launches.store(0); }
 
 static size_t ws_bytes_impl(int op, int d, const int64_t* dims, int64_t Id_global, int R, const int* ranks) {
+  if (op == KRP_OP_TTM && dims && d >= 2 && d <= kMaxD && R >= 1) {  // R = J; only mode 0 takes workspace
+    for (int k = 0; k < d; ++k)
+      if (dims[k] < 1) return 0;
+    return ttm_ws_bytes(make_dims(d, dims), 0, R) + 256;
+  }
   if (!dims || d < 2 || d > kMaxD || R < 1 || R > kMaxR) return 0;
   for (int k = 0; k < d; ++k)
     if (dims[k] < 1) return 0;
@@ -933,6 +941,25 @@ int krp_sketch_mode(const float* X, int d, const int64_t* dims, int n, const flo
   WsGuard guard;
   KRP_TRY(setup_arena(krp_workspace_bytes(KRP_OP_SKETCH_MODE, d, dims, R, nullptr), ws, ws_bytes, s, ar, guard));
   return sketch(X, g, make_om(omega, d, n), R, want, Yp, ar, s);
+}
+
+int krp_ttm(const float* X, int d, const int64_t* dims, int n, const float* A, int J, float* Y, void* ws,
+            size_t ws_bytes, void* stream) {
+  KRP_TRY(validate_common(X, d, dims, 1));
+  if (n < 0 || n >= d) {
+    set_error("mode n=%d not in [0,%d)", n, d);
+    return KRP_EINVAL;
+  }
+  if (!A || !Y || J < 1 || J > (1 << 24)) {
+    set_error("krp_ttm: A / Y NULL or J=%d not in [1, 2^24]", J);
+    return KRP_EINVAL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const Dims g = make_dims(d, dims);
+  Arena ar;
+  WsGuard guard;
+  KRP_TRY(setup_arena(krp_workspace_bytes(KRP_OP_TTM, d, dims, J, nullptr), ws, ws_bytes, s, ar, guard));
+  return ttm(X, g, n, A, J, g.n[n], 1, Y, s, &ar);
 }
 
 int krp_rhosvd(const float* X, int d, const int64_t* dims, const int* ranks, int R, const float* const* omega,

@@ -8,6 +8,8 @@ namespace krp {
 // Y_k are produced.  R in [1, 256] (column groups of <= 64 per launch).  KRP_EUNSUPPORTED (nothing
 // launched) on a device that is not sm_100a.
 bool tc_device_ok();
+void* tma_encode_fn();  // the driver's cuTensorMapEncodeTiled (PFN_cuTensorMapEncodeTiled_v12000)
+int device_sms();       // SM count of the current device
 size_t tc_sketch_ws_bytes(const Dims& g, int R, const bool* want_mode);
 int tc_sketch(const float* X, const Dims& g, const OmegaPtrs& om, int R, const bool* want_mode, float* const* Y,
               Arena& ar, cudaStream_t s);
@@ -37,8 +39,18 @@ size_t cholqr_ws_bytes(int64_t rows, int R);
 int cholqr(const float* Y, int64_t rows, int R, float* Qf, double* Qd, int* flag_dev, Arena& ar, cudaStream_t s);
 
 // Y = X x_n A for X of dims g (fp32), A: J x I_n with element (j, i) at A[j*sj + i*si] (fp32).
+// With an arena holding ttm_ws_bytes(g, n, J), mode 0 runs on the tensor cores (ttm0_tc, 3xTF32);
+// otherwise (and for every other mode) on the fp32 FMA kernels.
+size_t ttm_ws_bytes(const Dims& g, int n, int J);
 int ttm(const float* X, const Dims& g, int n, const float* A, int J, int64_t sj, int64_t si, float* Y,
-        cudaStream_t s);
+        cudaStream_t s, Arena* ar = nullptr);
+
+// ---- mode-0 TTM on tcgen05 (krp_ttm_tc.cu): Y[j + J h] = sum_i A[j sj + i si] X[i + I h], J <= 64,
+// I % 4 == 0, X 16-byte aligned; workspace: the B-operand image of A
+bool ttm0_tc_ok(const float* X, int64_t I, int64_t H, int J);
+size_t ttm0_tc_ws_bytes(int64_t I, int J);
+int ttm0_tc(const float* X, int64_t I, int64_t H, const float* A, int J, int64_t sj, int64_t si, float* Y, Arena& ar,
+            cudaStream_t s);
 
 // H = T_(n) T_(n)^T (J x J, fp64) for T of dims g with J = g.n[n].
 size_t mode_gram_ws_bytes(const Dims& g, int n);

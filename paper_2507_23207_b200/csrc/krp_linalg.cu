@@ -810,11 +810,17 @@ int cholqr(const float* Y, int64_t rows, int R, float* Qf, double* Qd, int* flag
   return KRP_OK;
 }
 
+size_t ttm_ws_bytes(const Dims& g, int n, int J) {
+  return (n == 0 && J >= 1 && J <= 64 && g.n[0] % 4 == 0) ? ttm0_tc_ws_bytes(g.n[0], J) : 0;
+}
+
 int ttm(const float* X, const Dims& g, int n, const float* A, int J, int64_t sj, int64_t si, float* Y,
-        cudaStream_t s) {
+        cudaStream_t s, Arena* ar) {
   const int64_t L = g.stride[n], I = g.n[n], H = g.N / (L * I);
   const int64_t P = L * H;
   if (P == 0 || J == 0) return KRP_OK;
+  if (ar && L == 1 && ttm0_tc_ok(X, I, H, J) && (ar->cap - ar->off) >= ttm0_tc_ws_bytes(I, J))
+    return ttm0_tc(X, I, H, A, J, sj, si, Y, *ar, s);
   if (L == 1 && J <= 64 && I % 4 == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 && H >= 148 * kQCols / 8) {
     switch ((J + 3) / 4) {
       case 1: return launch_ttm_mode0q<1>(X, I, H, A, J, sj, si, Y, s);

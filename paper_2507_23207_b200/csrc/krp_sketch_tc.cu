@@ -1304,6 +1304,8 @@ int tc_sketch_cols(const float* X, const Dims& g, const OmegaPtrs& om, int R, in
 }  // namespace
 
 bool tc_device_ok() { return device_is_sm100() && get_encode() != nullptr; }
+void* tma_encode_fn() { return reinterpret_cast<void*>(get_encode()); }
+int device_sms() { return num_sms(); }
 
 // Columns of a KRP sketch are independent (Lemma 2.3): R > 64 runs as column groups of <= 64
 // columns (one pass over X each), Ω and Y addressed through their row stride R.

@@ -180,6 +180,64 @@ def test_sketch_is_deterministic(krp):
         assert torch.equal(u, v)
 
 
+# ----------------------------------------------------------------- the core contraction (mode-n product)
+# Mode 0 with I_1 % 4 == 0 and J <= 64 runs on the tcgen05 3xTF32 kernel; the shapes below span several
+# 128-column tiles with a ragged last tile, K chunks with a ragged tail (I_1 = 36, 100), J = 1 .. 64 and
+# the N padding (J = 10, 30, 50); the other modes / I_1 % 4 != 0 take the fp32 FMA kernels.
+TTM_CASES = [((128, 40, 33), 0, 30), ((36, 50, 7), 0, 1), ((100, 77, 5), 0, 50), ((64, 64, 64), 0, 64),
+             ((32, 17, 3, 5), 0, 10), ((2048, 20, 9), 0, 60), ((30, 40, 20), 0, 20), ((40, 36, 20), 1, 30),
+             ((24, 20, 36), 2, 12)]
+
+
+@pytest.mark.parametrize("dims,n,J", TTM_CASES)
+def test_ttm_vs_oracle(krp, dims, n, J):
+    x = synth.random_tensor(dims, 31)
+    a = np.random.default_rng([31, n, J]).standard_normal((J, dims[n])).astype(np.float32)
+    y = krp.krp_ttm(_dev(x), dims, n, _dev(a)).cpu().numpy()
+    out = list(dims)
+    out[n] = J
+    ref = oracle.ttm(oracle.as_tensor(x, dims), a, n)
+    got = oracle.as_tensor(y, out)
+    assert rel(got, ref) <= Y_TOL, rel(got, ref)
+    # every element within a conservative 3xTF32 bound: per product the dropped lo*lo term and the tf32
+    # rounding of the two lo operands (each < 2^-20 |a x| even for a truncating split), plus fp32
+    # accumulation over I_n terms (gamma_I ~ I 2^-24), relative to its own scale sum_i |a_ji x_i|
+    scale = oracle.ttm(np.abs(oracle.as_tensor(x, dims)), np.abs(a.astype(np.float64)), n)
+    bound = (3 * 2.0 ** -20 + dims[n] * 2.0 ** -24) * scale
+    assert np.all(np.abs(got - ref) <= bound + 1e-30)
+
+
+def test_ttm_positive_data_has_bounded_rounding_bias(krp):
+    """All-positive X and A (the c5 smooth tensor against its dominant factor column): rounding errors of one
+    sign add coherently here.  Two sources are bounded by the kernel's design: a truncating tf32 split would
+    drop ~3 2^-22 = 7e-7 relative (the kernel splits round-to-nearest), and the tensor core's accumulation
+    into TMEM rounds toward zero (~0.6 ulp per accumulating MMA: 4.6e-6 low for K = 512 accumulated in
+    TMEM), so accumulators hold one 32-wide K chunk (4 MMAs, ~1.4e-7) and chunks are summed in fp32
+    round-to-nearest registers."""
+    dims, J = (512, 300, 4), 16
+    i, j, k = np.meshgrid(*[np.arange(n, dtype=np.float64) for n in dims], indexing="ij")
+    x = (1.0 / (1.0 + i / dims[0] + j / dims[1] + k / dims[2])).reshape(-1, order="F").astype(np.float32)
+    a = np.random.default_rng(11).uniform(0.1, 1.0, (J, dims[0])).astype(np.float32)
+    y = krp.krp_ttm(_dev(x), dims, 0, _dev(a)).cpu().numpy()
+    ref = oracle.ttm(oracle.as_tensor(x, dims), a, 0)
+    assert rel(oracle.as_tensor(y, (J,) + dims[1:]), ref) <= 3e-7
+
+
+def test_ttm_tensor_core_is_exact_on_small_integers_and_deterministic(krp):
+    """Small integers are tf32-exact (lo = 0) with integer partial sums < 2^24: bit-exact; and a repeat is
+    bit-identical (fixed summation order)."""
+    dims, J = (96, 300, 3), 40
+    g = np.random.default_rng(5)
+    x = g.integers(-3, 4, int(np.prod(dims))).astype(np.float32)
+    a = g.integers(-2, 3, (J, dims[0])).astype(np.float32)
+    y = krp.krp_ttm(_dev(x), dims, 0, _dev(a))
+    ref = oracle.ttm(oracle.as_tensor(x, dims), a, 0)
+    assert np.array_equal(oracle.as_tensor(y.cpu().numpy(), (J, 300, 3)), ref)
+    xr = _dev(synth.random_tensor(dims, 6))
+    ar = _dev(g.standard_normal((J, dims[0])))
+    assert torch.equal(krp.krp_ttm(xr, dims, 0, ar), krp.krp_ttm(xr, dims, 0, ar))
+
+
 # ----------------------------------------------------------------- rHOSVD / STHOSVD
 def _check_factors(Q, ranks, tol=QTQ_TOL):
     for q, r in zip(Q, ranks):
