@@ -42,7 +42,7 @@ __all__ = [
     "thin_qr",
     "ttm",
     "multi_ttm",
-    "leading_left_singular_vectors",
+    "leading_left_singular_vectors", "canonical_signs",
     "rhosvd",
     "sthosvd",
     "reconstruct",
@@ -222,10 +222,24 @@ def multi_ttm(x: np.ndarray, mats: Sequence[Optional[np.ndarray]]) -> np.ndarray
     return y
 
 
+def canonical_signs(u: np.ndarray) -> np.ndarray:
+    """Columns signed so that each column's entry of largest magnitude (first on ties) is positive
+    (reading R24: singular vectors are defined up to sign; STHOSVD's later sketches
+    pair the rows of Omega_j with the basis chosen at step j (R5), so both sides fix the sign the
+    same way)."""
+    u = np.array(u, dtype=np.float64, copy=True)
+    for t in range(u.shape[1]):
+        i = int(np.argmax(np.abs(u[:, t])))
+        if u[i, t] < 0:
+            u[:, t] = -u[:, t]
+    return u
+
+
 def leading_left_singular_vectors(m: np.ndarray, r: int) -> Tuple[np.ndarray, np.ndarray]:
-    """U(:, 1:r) and the singular values of M (LAPACK SVD), Alg. 2 line 2-3 pattern."""
+    """U(:, 1:r) and the singular values of M (LAPACK SVD), Alg. 2 line 2-3 pattern, signs
+    canonical (reading R24)."""
     u, s, _ = np.linalg.svd(np.asarray(m, dtype=np.float64), full_matrices=False)
-    return u[:, :r], s
+    return canonical_signs(u[:, :r]), s
 
 
 # ----------------------------------------------------------------- Tucker algorithms

@@ -550,11 +550,19 @@ MGPlan plan_mode_gram(const Dims& g, int n) {
 }
 
 // ------------------------------------------------------------------ symmetric eigensolver (Jacobi)
-// Parallel cyclic Jacobi (round-robin pairing: m-1 rounds of m/2 disjoint rotations per sweep).  One
-// round's update is ONE phase: thread (ki, kj) owns the 2x2 block of rows {p_ki, q_ki} x columns
-// {p_kj, q_kj}; it reads the two rotations from shared memory, writes the block of J^T A J into the
-// other A buffer and rotates its 2x2 block of V in place.  The m/2 rotations of a round are computed once
-// (fp64 divide/sqrt throughput makes per-block recomputation slower), so a round is two phases.
+// One-sided (Hestenes) cyclic Jacobi on the symmetric PSD Gram matrix H: right rotations A <- A J, V <- V J
+// (A = H initially) until the columns of A = H V are mutually orthogonal; then H V = V Λ, so the columns
+// of V are the eigenvectors and ||a_i|| = λ_i.  Round-robin pairing (m-1 rounds of m/2 disjoint pairs per
+// sweep, tabulated in shared memory once); ONE HALF-WARP PER PAIR: 16 lanes hold columns p, q of A and V
+// (rows l, l+16, l+32, l+48 per lane: each half-warp access is one conflict-free 128-byte wavefront),
+// form α = a_p·a_p, β = a_q·a_q, γ = a_p·a_q by xor-butterfly reductions (all 16 lanes end with
+// bit-identical sums, so they form the same rotation), rotate, and write the columns back in place (a
+// round's pairs are disjoint: no double buffer).  One named barrier per round.  The round is issue-bound
+// (the SM runs m/4 warps of ~160 instructions each), so the rotation uses fast fp32 approximations for the
+// ANGLE only; (c, s) are renormalised in fp64 (c^2 + s^2 = 1 to fp64 rounding), so every update is an
+// exact-to-rounding orthogonal rotation and V stays orthogonal; an approximate angle leaves γ' ~ 1e-6 γ,
+// which the next sweep removes.  A pair is rotated while γ^2 > (1e-13)^2 αβ (above the ~m·u rounding
+// floor of the dot products); the sweep loop ends after a sweep without rotations.
 __device__ __forceinline__ void jacobi_pair(int round, int k, int m, int& p, int& q) {
   int a, b;
   if (k == 0) {
@@ -568,18 +576,43 @@ __device__ __forceinline__ void jacobi_pair(int round, int k, int m, int& p, int
   q = a < b ? b : a;
 }
 
-__device__ __forceinline__ void jacobi_rot(const double (*A)[kGramMaxR + 1], int p, int q, int J, double& c,
-                                           double& s) {
-  c = 1.0;
-  s = 0.0;
-  if (q < J && A[p][q] != 0.0) {
-    // t = sign(tau) / (|tau| + sqrt(1 + tau^2)) with tau = x / y, x = a_qq - a_pp, y = 2 a_pq, written
-    // with one divide: t = sign(x) y / (|x| + sqrt(x^2 + y^2))  (sign(0) = +1)
-    const double x = A[q][q] - A[p][p], y = 2.0 * A[p][q];
-    const double t = (x >= 0.0 ? y : -y) / (fabs(x) + sqrt(fma(x, x, y * y)));
-    c = rsqrt(fma(t, t, 1.0));
-    s = t * c;
+// (c, s) of the rotation orthogonalising columns with Gram [[α, γ], [γ, β]]: t = sign(x) y / (|x| +
+// sqrt(x^2 + y^2)) with x = β - α, y = 2γ (sign(0) = +1), c = 1 / sqrt(1 + t^2), s = t c; the pair is
+// then a_p' = c a_p - s a_q, a_q' = s a_p + c a_q.
+__device__ __forceinline__ void jacobi_rot(double alpha, double beta, double gamma, double& c, double& s) {
+  double x = beta - alpha, y = 2.0 * gamma;
+  // scale by a power of two so that the larger of |x|, |y| is in [1, 2): no fp32 overflow / underflow
+  const double mx = fmax(fabs(x), fabs(y));
+  const int e = static_cast<int>((__double_as_longlong(mx) >> 52) & 0x7FF) - 1023;
+  const double sc = __longlong_as_double(static_cast<long long>(1023 - e) << 52);
+  x *= sc;
+  y *= sc;
+  const float xf = static_cast<float>(x), yf = static_cast<float>(y);
+  const float r2 = fmaf(xf, xf, yf * yf);
+  const float tf = __fdividef(xf >= 0.f ? yf : -yf, fabsf(xf) + r2 * rsqrtf(r2));
+  const float cf = rsqrtf(fmaf(tf, tf, 1.f));
+  double cd = static_cast<double>(cf), sd = static_cast<double>(tf * cf);
+  // two Newton steps for 1/sqrt(n), n = c^2 + s^2 = 1 + O(1e-6): |c^2 + s^2 - 1| -> O(1e-16)
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const double n = fma(cd, cd, sd * sd);
+    const double f = fma(-0.5, n, 1.5);
+    cd *= f;
+    sd *= f;
   }
+  c = cd;
+  s = sd;
+}
+
+__device__ __forceinline__ double halfwarp_sum_f64(double v) {
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum_f64(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
 }
 
 struct EigBatch {
@@ -588,121 +621,129 @@ struct EigBatch {
   int r[kMaxD];
 };
 
-// one problem per block: blockIdx.x selects (H, r, U) of the batch
+// one problem per block (blockIdx.x selects (H, r, U) of the batch); columns stored contiguously:
+// A[j * 64 + i] = a_j(i), V likewise, rows >= J zero
 __global__ void __launch_bounds__(1024) jacobi_top_kernel(EigBatch batch, int J) {
   const double* __restrict__ Hm = batch.H[blockIdx.x];
   float* __restrict__ U = batch.U[blockIdx.x];
   const int r = batch.r[blockIdx.x];
   extern __shared__ double dyn_smem[];
-  typedef double Row[kGramMaxR + 1];
-  Row* Abuf[2] = {reinterpret_cast<Row*>(dyn_smem), reinterpret_cast<Row*>(dyn_smem + kGramMaxR * (kGramMaxR + 1))};
-  Row* V = reinterpret_cast<Row*>(dyn_smem + 2 * kGramMaxR * (kGramMaxR + 1));
-  __shared__ double offn, totn;
+  double* A = dyn_smem;                  // [64][64]
+  double* V = dyn_smem + 64 * 64;        // [64][64]
+  __shared__ uint16_t ptab[kGramMaxR - 1][kGramMaxR / 2];  // round-robin pairs: p | q << 8
+  __shared__ double lam[kGramMaxR];
   __shared__ int order[kGramMaxR];
-  __shared__ double part_off[32], part_tot[32];
-  __shared__ double cs[kGramMaxR / 2], sn[kGramMaxR / 2];
-  __shared__ int pp[kGramMaxR / 2], qq[kGramMaxR / 2];
-  const int tid = threadIdx.x;
-  const int m = J + (J & 1);  // even number of players; index J (if odd J) is a dummy
+  __shared__ int rotated[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int m = J + (J & 1);  // even number of players; column J (if odd J) is a zero dummy
   const int half = m / 2;
-  const bool owner = tid < half * half;
-  const int ki = owner ? tid / half : 0, kj = owner ? tid % half : 0;
-  for (int e = tid; e < J * J; e += blockDim.x) {
-    const int i = e / J, j = e % J;
-    Abuf[0][i][j] = Hm[e];
-    V[i][j] = (i == j) ? 1.0 : 0.0;
+  const int nwork = (half + 1) / 2;  // warps with a pair in either half
+  for (int e = tid; e < (m - 1) * half; e += blockDim.x) {
+    int p, q;
+    jacobi_pair(e / half, e % half, m, p, q);
+    ptab[e / half][e % half] = static_cast<uint16_t>(p | (q << 8));
+  }
+  for (int e = tid; e < 64 * 64; e += blockDim.x) {
+    const int j = e >> 6, i = e & 63;
+    A[e] = (i < J && j < J) ? Hm[i * J + j] : 0.0;  // H symmetric: column j = row j
+    V[e] = (i == j) ? 1.0 : 0.0;
+  }
+  if (tid < 2) rotated[tid] = 0;
+  __syncthreads();
+  const int k = 2 * warp + (lane >> 4);  // this half-warp's pair slot
+  const int l = lane & 15;
+#ifdef KRP_DEV_TRACE
+  int dev_sweeps = 0;
+#endif
+  for (int sweep = 0; sweep < 30 && m >= 2; ++sweep) {
+#ifdef KRP_DEV_TRACE
+    dev_sweeps = sweep + 1;
+#endif
+    const int flag = sweep & 1;  // rotated[flag] collects this sweep; rotated[flag ^ 1] is reset for the next
+    if (warp < nwork) {
+      for (int round = 0; round < m - 1; ++round) {
+        const bool act = k < half;
+        const int pq = act ? ptab[round][k] : 0;
+        double* ap = A + (pq & 0xFF) * 64 + l;
+        double* aq = A + (pq >> 8) * 64 + l;
+        double pv[4], qv[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          pv[t] = act ? ap[16 * t] : 0.0;
+          qv[t] = act ? aq[16 * t] : 0.0;
+        }
+        double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          al = fma(pv[t], pv[t], al);
+          be = fma(qv[t], qv[t], be);
+          ga = fma(pv[t], qv[t], ga);
+        }
+        al = halfwarp_sum_f64(al);
+        be = halfwarp_sum_f64(be);
+        ga = halfwarp_sum_f64(ga);
+        if (act && ga * ga > 1e-26 * (al * be)) {  // uniform within the half-warp
+          double c, sn;
+          jacobi_rot(al, be, ga, c, sn);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            ap[16 * t] = c * pv[t] - sn * qv[t];
+            aq[16 * t] = sn * pv[t] + c * qv[t];
+          }
+          double* vp = V + (pq & 0xFF) * 64 + l;
+          double* vq = V + (pq >> 8) * 64 + l;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const double v0 = vp[16 * t], w0 = vq[16 * t];
+            vp[16 * t] = c * v0 - sn * w0;
+            vq[16 * t] = sn * v0 + c * w0;
+          }
+          if (l == 0) rotated[flag] = 1;
+        }
+        // all pairs of this round are done before the next round re-pairs the columns
+        asm volatile("bar.sync 1, %0;" ::"r"(nwork * 32) : "memory");
+      }
+    }
+    __syncthreads();
+    const bool again = rotated[flag] != 0;
+    if (tid == 0) rotated[flag ^ 1] = 0;
+    __syncthreads();
+    if (!again) break;
+  }
+#ifdef KRP_DEV_TRACE
+  if (tid == 0) printf("jacobi block %d J=%d: %d sweeps\n", blockIdx.x, J, dev_sweeps);
+#endif
+  // λ_j = ||a_j|| (fixed-order warp sums), then the r largest, descending
+  for (int j = warp; j < J; j += blockDim.x >> 5) {
+    const double a0 = A[j * 64 + lane], a1 = A[j * 64 + lane + 32];
+    const double n2 = warp_sum_f64(fma(a0, a0, a1 * a1));
+    if (lane == 0) lam[j] = sqrt(n2);
   }
   __syncthreads();
-  int cur = 0;
-  for (int sweep = 0; sweep < 40; ++sweep) {
-    {  // off-diagonal and total squared norms: per-thread partial sums, then a fixed-order warp tree
-      const Row* A = Abuf[cur];
-      double off = 0.0, tot = 0.0;
-      for (int e = tid; e < 64 * 64; e += blockDim.x) {
-        const int i = e >> 6, j = e & 63;
-        if (i >= J || j >= J) continue;
-        const double v = A[i][j] * A[i][j];
-        tot += v;
-        if (i != j) off += v;
-      }
-      for (int o = 16; o > 0; o >>= 1) {
-        off += __shfl_xor_sync(0xffffffffu, off, o);
-        tot += __shfl_xor_sync(0xffffffffu, tot, o);
-      }
-      if ((tid & 31) == 0) {
-        part_off[tid >> 5] = off;
-        part_tot[tid >> 5] = tot;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        double so = 0.0, st = 0.0;
-        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) so += part_off[w], st += part_tot[w];
-        offn = so;
-        totn = st;
-      }
-      __syncthreads();
-    }
-    // converged when the off-diagonal mass is ~(1e-13)^2 of the total: eigenvectors are then accurate
-    // far below the fp32 output precision
-    if (!(offn > 1e-26 * totn) || m < 2) break;
-    for (int round = 0; round < m - 1; ++round) {
-      if (tid < half) {  // the round's m/2 rotations, once each
-        int p, q;
-        jacobi_pair(round, tid, m, p, q);
-        jacobi_rot(Abuf[cur], p, q, J, cs[tid], sn[tid]);
-        pp[tid] = p;
-        qq[tid] = q;
-      }
-      __syncthreads();
-      if (owner) {
-        const Row* A = Abuf[cur];
-        Row* An = Abuf[cur ^ 1];
-        const int pi = pp[ki], qi = qq[ki], pj = pp[kj], qj = qq[kj];
-        const double ci = cs[ki], si = sn[ki], cj = cs[kj], sj = sn[kj];
-        const bool qiv = qi < J, qjv = qj < J;  // pi, pj < J always (the dummy is the larger index)
-        const double a00 = A[pi][pj];
-        const double a01 = qjv ? A[pi][qj] : 0.0;
-        const double a10 = qiv ? A[qi][pj] : 0.0;
-        const double a11 = (qiv && qjv) ? A[qi][qj] : 0.0;
-        // rows: A <- J^T A, then columns: A <- A J (the order of the two-phase formulation)
-        const double b00 = ci * a00 - si * a10, b01 = ci * a01 - si * a11;
-        const double b10 = si * a00 + ci * a10, b11 = si * a01 + ci * a11;
-        An[pi][pj] = cj * b00 - sj * b01;
-        if (qjv) An[pi][qj] = sj * b00 + cj * b01;
-        if (qiv) An[qi][pj] = cj * b10 - sj * b11;
-        if (qiv && qjv) An[qi][qj] = sj * b10 + cj * b11;
-        // V <- V J: rows {pi, qi}, columns {pj, qj}
-        if (qjv) {
-          const double vp = V[pi][pj], vq = V[pi][qj];
-          V[pi][pj] = cj * vp - sj * vq;
-          V[pi][qj] = sj * vp + cj * vq;
-          if (qiv) {
-            const double wp = V[qi][pj], wq = V[qi][qj];
-            V[qi][pj] = cj * wp - sj * wq;
-            V[qi][qj] = sj * wp + cj * wq;
-          }
-        }
-      }
-      cur ^= 1;
-      __syncthreads();
-    }
-  }
-  const Row* A = Abuf[cur];
   if (tid == 0) {
     for (int i = 0; i < J; ++i) order[i] = i;
-    for (int t = 0; t < r; ++t) {  // selection of the r largest eigenvalues, descending
+    for (int t = 0; t < r; ++t) {
       int best = t;
       for (int i = t + 1; i < J; ++i)
-        if (A[order[i]][order[i]] > A[order[best]][order[best]]) best = i;
+        if (lam[order[i]] > lam[order[best]]) best = i;
       const int tmp = order[t];
       order[t] = order[best];
       order[best] = tmp;
     }
   }
   __syncthreads();
+  // canonical signs (reading R24): each eigenvector's entry of largest magnitude (first on ties) positive
+  for (int t = tid; t < r; t += blockDim.x) {
+    const double* v = V + order[t] * 64;
+    int best = 0;
+    for (int i = 1; i < J; ++i)
+      if (fabs(v[i]) > fabs(v[best])) best = i;
+    lam[t] = v[best] < 0.0 ? -1.0 : 1.0;  // lam is free again: reused for the signs
+  }
+  __syncthreads();
   for (int e = tid; e < J * r; e += blockDim.x) {
     const int i = e / r, t = e % r;
-    U[e] = static_cast<float>(V[i][order[t]]);
+    U[e] = static_cast<float>(lam[t] * V[order[t] * 64 + i]);
   }
 }
 

@@ -8,18 +8,20 @@
 //
 // As a GEMM: Yᵀ (H x J) = X_(1)ᵀ (H x I, K-major: i contiguous) · Aᵀ.  M = 128 columns h per tile, N = J
 // (padded to Np = round16(J) <= 64), K = I in chunks of 32 (one TMA box {32 i, 128 h}, SWIZZLE_128B,
-// out-of-range i / h zero-filled).  3xTF32 with ROUND-TO-NEAREST splits: hi = rn_tf32(x), lo = rn_tf32(x - hi),
-// so x = hi + lo + e with |e| <= 2^-22 |x| of either sign, and the dropped lo·lo term (<= 2^-22 |x a|) has
+// out-of-range i / h zero-filled).  3xTF32 with a ROUND-TO-NEAREST split: hi = rn_tf32(x) (two integer
+// ops on the bits), lo = x - hi exactly (fp32), which the tensor core reads truncated to tf32; lo has
+// either sign, so the truncation of lo (<= 2^-22 |x|) and the dropped lo·lo term (<= 2^-22 |x a|) have
 // either sign too.  (The sketch kernel's truncation split, hi = the raw value as the tensor core reads it,
 // leaves lo with the sign of x: on a positive tensor such as c5's the dropped terms then add coherently, a
 // ~1e-6 relative bias of every core entry, which is the size of c5's whole Tucker error.)
-//     D1 = X_hi · [A_hi | A_lo]ᵀ   (N = 2Np: columns hh | hl)
-//     D2 = X_lo · A_hiᵀ            (N = Np: lh)
+//     D[0, 2Np)   = X_hi · [A_hi | A_lo]ᵀ   (N = 2Np: columns hh | hl)
+//     D[Np, 2Np) += X_lo · A_hiᵀ            (N = Np: the two small cross terms share columns)
 // both with the A operand in TMEM (written by the split warps).  The tensor core's fp32 accumulation into
 // TMEM rounds toward zero (measured: a positive K = 512 product came out 4.6e-6 low, ~0.6 ulp per
-// accumulating MMA), so the accumulators hold ONE K chunk (4 accumulating MMAs) and are drained every
-// chunk: the epilogue warps add hh + (hl + lh) of each chunk into fp32 registers with round-to-nearest
-// adds, in chunk order.  The B operand [A_hi | A_lo] of every K chunk is
+// accumulating MMA), so the accumulators hold ONE K chunk (4 accumulating MMAs on the hh columns) and are
+// drained every chunk: the epilogue warps add hh + (hl + lh) of each chunk into fp32 registers with
+// round-to-nearest adds, in chunk order (the cross-term columns are 2^-11 smaller: their own rounding
+// bias is negligible).  The B operand [A_hi | A_lo] of every K chunk is
 // prepared once per call (a tiny kernel) as the exact shared-memory image (rows of 128 B, 128B swizzle)
 // and streamed next to each X box by a bulk copy (it stays in L2: <= 1 MB).
 //
@@ -47,7 +49,7 @@ constexpr int kT0Rows = 128;   // tile: 128 columns h
 constexpr int kT0K = 32;       // K chunk: one 128-byte row of the TMA box
 constexpr int kT0SlotCols = 64;  // TMEM columns of one chunk slot: X_hi [0, 32), X_lo [32, 64)
 constexpr int kT0MaxNC = 4;    // chunk slots (X_hi | X_lo), as many as TMEM leaves room for
-constexpr int kT0NA = 2;       // chunk accumulator stages, 3 Np columns each (hh | hl | lh)
+constexpr int kT0NA = 2;       // chunk accumulator stages, 2 Np columns each (hh | hl + lh)
 constexpr int kT0MaxJ = 64;
 
 struct Ttm0Params {
@@ -68,6 +70,10 @@ __device__ __forceinline__ uint32_t tf32_rn_bits(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return r;
 }
+
+// round to the nearest tf32 on the bits (ties away from zero: +half an ulp of tf32 on the magnitude, then
+// clear the 13 low mantissa bits); finite inputs (an infinity becomes a NaN, which it would produce anyway)
+__device__ __forceinline__ uint32_t tf32_rn_fast(uint32_t u) { return (u + 0x1000u) & 0xFFFFE000u; }
 
 // B image: element (row n, k) of chunk kc at byte kc * 2Np*128 + sw128_offset(n, k)
 __global__ void ttm0_bimg_kernel(const float* __restrict__ A, int J, int I, int64_t sj, int64_t si, int Np, int nk,
@@ -137,7 +143,7 @@ __global__ void __launch_bounds__(kT0Threads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  const uint32_t tm_slot = static_cast<uint32_t>(kT0NA * 3 * p.Np);  // chunk slots after the accumulators
+  const uint32_t tm_slot = static_cast<uint32_t>(kT0NA * 2 * p.Np);  // chunk slots after the accumulators
 
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * p.T / gridDim.x;
   const int64_t t1 = static_cast<int64_t>(blockIdx.x + 1) * p.T / gridDim.x;
@@ -178,14 +184,14 @@ __global__ void __launch_bounds__(kT0Threads, 1)
         T0WAIT(&full[st], ph);
         T0WAIT(&lo_full[cs], cph);
         tc_fence_after();
-        const uint32_t d1 = tbase + static_cast<uint32_t>(as * 3 * p.Np), d2 = d1 + 2 * p.Np;
+        const uint32_t d1 = tbase + static_cast<uint32_t>(as * 2 * p.Np), d2 = d1 + p.Np;
         const uint64_t bd = bdesc0 + ((static_cast<uint64_t>(st) * p.b_bytes) >> 4);
         const uint32_t thi = tbase + tm_slot + static_cast<uint32_t>(cs * kT0SlotCols);
         if (leader) {
 #pragma unroll
           for (int ks = 0; ks < kT0K / 8; ++ks) {  // K = 8 per MMA: +32 B on the B descriptor's start address
             mma_tf32_ts(d1, thi + 8 * ks, bd + ks * 2, idesc_cat, ks ? 1u : 0u);       // hi x [A_hi | A_lo]
-            mma_tf32_ts(d2, thi + 32 + 8 * ks, bd + ks * 2, idesc_lo, ks ? 1u : 0u);   // lo x A_hi
+            mma_tf32_ts(d2, thi + 32 + 8 * ks, bd + ks * 2, idesc_lo, 1u);             // lo x A_hi
           }
           mma_commit(&empty[st]);
           mma_commit(&lo_free[cs]);
@@ -230,9 +236,13 @@ __global__ void __launch_bounds__(kT0Threads, 1)
         }
         uint32_t hv[kT0K];
 #pragma unroll
-        for (int k = 0; k < kT0K; ++k) {
-          hv[k] = tf32_rn_bits(__uint_as_float(v[k]));
-          v[k] = tf32_rn_bits(__uint_as_float(v[k]) - __uint_as_float(hv[k]));
+        for (int k = 0; k < kT0K; k += 2) {
+          hv[k] = tf32_rn_fast(v[k]);
+          hv[k + 1] = tf32_rn_fast(v[k + 1]);
+          const float2 l = f2_sub(make_float2(__uint_as_float(v[k]), __uint_as_float(v[k + 1])),
+                                  make_float2(__uint_as_float(hv[k]), __uint_as_float(hv[k + 1])));
+          v[k] = __float_as_uint(l.x);
+          v[k + 1] = __float_as_uint(l.y);
         }
         const uint32_t slot = tbase + lane_off + tm_slot + static_cast<uint32_t>(cs * kT0SlotCols);
         tmem_st<32>(slot, hv);
@@ -269,18 +279,22 @@ __global__ void __launch_bounds__(kT0Threads, 1)
       for (int kc = 0; kc < nk; ++kc) {
         T0WAIT(&acc_full[as], aph);
         tc_fence_after();
-        const uint32_t d1 = tbase + lane_off + static_cast<uint32_t>(as * 3 * Np);
+        const uint32_t d1 = tbase + lane_off + static_cast<uint32_t>(as * 2 * Np);
 #pragma unroll
         for (int c = 0; c < kT0MaxJ; c += 16) {
           if (c < Np) {
-            uint32_t hh[16], hl[16], lh[16];
+            uint32_t hh[16], hl[16];
             tmem_ld<16>(d1 + c, hh);
             tmem_ld<16>(d1 + Np + c, hl);
-            tmem_ld<16>(d1 + 2 * Np + c, lh);
             tmem_ld_wait();
 #pragma unroll
-            for (int k = 0; k < 16; ++k)
-              acc[c + k] += __uint_as_float(hh[k]) + (__uint_as_float(hl[k]) + __uint_as_float(lh[k]));
+            for (int k = 0; k < 16; k += 2) {
+              const float2 t = f2_add(make_float2(__uint_as_float(hh[k]), __uint_as_float(hh[k + 1])),
+                                      make_float2(__uint_as_float(hl[k]), __uint_as_float(hl[k + 1])));
+              const float2 a2 = f2_add(make_float2(acc[c + k], acc[c + k + 1]), t);
+              acc[c + k] = a2.x;
+              acc[c + k + 1] = a2.y;
+            }
           }
         }
         tc_fence_before();
@@ -361,7 +375,7 @@ int ttm0_tc(const float* X, int64_t I, int64_t H, const float* A, int J, int64_t
   p.sm_stg = p.sm_b + p.NS * p.b_bytes;
   p.sm_bar = p.sm_stg + stg_bytes;
   const uint32_t smem_bytes = p.sm_bar + (2 * p.NS + 2 * kT0MaxNC + 2 * kT0NA) * 8 + 16 + 1024;
-  p.NC = std::min(kT0MaxNC, (512 - kT0NA * 3 * p.Np) / kT0SlotCols);  // TMEM: 2 x 3 Np + NC x 64 <= 512
+  p.NC = std::min(kT0MaxNC, (512 - kT0NA * 2 * p.Np) / kT0SlotCols);  // TMEM: 2 x 2 Np + NC x 64 <= 512
 
   CUtensorMap tmap;
   {

@@ -551,3 +551,21 @@ def test_hadamard_tucker_structured_equals_explicit():
 def _tk(f, g):
     from oracle.krp_oracle import _tensor_kron
     return _tensor_kron(np.asarray(f, dtype=np.float64), np.asarray(g, dtype=np.float64))
+
+
+def test_leading_singular_vectors_canonical_signs():
+    """Reading R24: U is LAPACK's left singular basis with each column's largest-magnitude entry made
+    positive.  Pins: the columns are the singular vectors (M M^T u = s^2 u against the eigen-decomposition
+    of M M^T), the sign rule holds, and flipping the input's sign pattern does not change U."""
+    m = np.random.default_rng(3).standard_normal((12, 40)) * np.logspace(0, -3, 12)[:, None]
+    u, s = oracle.leading_left_singular_vectors(m, 5)
+    g = m @ m.T
+    assert np.allclose(g @ u, u * s[:5] ** 2, rtol=1e-10, atol=1e-12 * s[0] ** 2)
+    w, v = np.linalg.eigh(g)
+    assert np.allclose(np.abs(u.T @ v[:, ::-1][:, :5]), np.eye(5), atol=1e-10)
+    for t in range(5):
+        i = int(np.argmax(np.abs(u[:, t])))
+        assert u[i, t] > 0
+    # any sign pattern LAPACK returns maps to the same canonical U
+    flip = oracle.canonical_signs(-u)
+    assert np.array_equal(flip, u)
