@@ -185,7 +185,29 @@ static int ttm_chain(const float* X, Dims g, const TtmOp* ops, float* bufA, floa
     return KRP_OK;
   }
   bool use_a = true;
-  for (int k = 0; k < g.d; ++k) {
+  int k_begin = 0;
+  // modes 1 and 2 both contracted on the tensor cores: the first product is written mode-permuted,
+  // (I_2, J_1, I_3..), so the second is again a mode-0 product, written permuted back to (J_1, J_2, I_3..)
+  if (ar && g.d >= 2 && ops[0].A && ops[1].A && last >= 1 && g.n[1] % 4 == 0 && ops[1].J <= 64 &&
+      ttm0_tc_ok(X, g.n[0], g.N / g.n[0], ops[0].J) &&
+      (ar->cap - ar->off) >= std::max(ttm0_tc_ws_bytes(g.n[0], ops[0].J), ttm0_tc_ws_bytes(g.n[1], ops[1].J))) {
+    const int64_t rest = g.N / (g.n[0] * g.n[1]);
+    float* t1 = bufA;
+    KRP_TRY(ttm0_tc(X, g.n[0], g.N / g.n[0], ops[0].A, ops[0].J, ops[0].sj, ops[0].si, t1, *ar, s, g.n[1]));
+    float* t2 = (last == 1) ? out : bufB;
+    KRP_TRY(ttm0_tc(t1, g.n[1], static_cast<int64_t>(ops[0].J) * rest, ops[1].A, ops[1].J, ops[1].sj, ops[1].si, t2,
+                    *ar, s, ops[0].J));
+    int64_t nd[kMaxD];
+    for (int m = 0; m < g.d; ++m) nd[m] = g.n[m];
+    nd[0] = ops[0].J;
+    nd[1] = ops[1].J;
+    g = make_dims(g.d, nd);
+    src = t2;
+    use_a = true;
+    k_begin = 2;
+    if (last == 1) return KRP_OK;
+  }
+  for (int k = k_begin; k < g.d; ++k) {
     if (!ops[k].A) continue;
     float* dst = (k == last) ? out : (use_a ? bufA : bufB);
     KRP_TRY(ttm(src, g, k, ops[k].A, ops[k].J, ops[k].sj, ops[k].si, dst, s, ar));
@@ -392,7 +414,8 @@ static int rhosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_t
     Dims cg = make_dims(d, cd);
     for (int k = 0; k < d; ++k) scratch = std::max(scratch, mode_gram_ws_bytes(cg, k));
   }
-  scratch = std::max(scratch, ttm_ws_bytes(g, 0, R));  // the first core contraction on the tensor cores
+  // the first two core contractions on the tensor cores (ttm_chain)
+  scratch = std::max(scratch, std::max(ttm_ws_bytes(g, 0, R), ttm0_tc_ws_bytes(g.n[1], R)));
   // error pass buffers: slab chunks of the last mode
   const int64_t inner = g.N / g.n[d - 1];
   int64_t chunk = std::max<int64_t>(1, (int64_t(1) << 25) / std::max<int64_t>(inner, 1));

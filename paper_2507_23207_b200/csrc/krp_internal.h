@@ -46,11 +46,13 @@ int ttm(const float* X, const Dims& g, int n, const float* A, int J, int64_t sj,
         cudaStream_t s, Arena* ar = nullptr);
 
 // ---- mode-0 TTM on tcgen05 (krp_ttm_tc.cu): Y[j + J h] = sum_i A[j sj + i si] X[i + I h], J <= 64,
-// I % 4 == 0, X 16-byte aligned; workspace: the B-operand image of A
+// I % 4 == 0, X 16-byte aligned; workspace: the B-operand image of A.  H1 > 0 (dividing H): the output is
+// written mode-permuted, Y[h1 + H1 (j + J h2)] for h = h1 + H1 h2, i.e. (I_2, J, I_3..) instead of
+// (J, I_2, I_3..), so the next contraction (over I_2) is again a mode-0 product.
 bool ttm0_tc_ok(const float* X, int64_t I, int64_t H, int J);
 size_t ttm0_tc_ws_bytes(int64_t I, int J);
 int ttm0_tc(const float* X, int64_t I, int64_t H, const float* A, int J, int64_t sj, int64_t si, float* Y, Arena& ar,
-            cudaStream_t s);
+            cudaStream_t s, int64_t H1 = 0);
 
 // H = T_(n) T_(n)^T (J x J, fp64) for T of dims g with J = g.n[n].
 size_t mode_gram_ws_bytes(const Dims& g, int n);

@@ -62,6 +62,7 @@ struct Ttm0Params {
   uint32_t b_bytes;  // one B image chunk: 2 Np rows x 128 B
   const float* Bimg; // [nk][2 Np][32] swizzled: rows [0, Np) A_hi, [Np, 2Np) A_lo
   float* Y;
+  int64_t H1;        // > 0: permuted output Y[h1 + H1 (j + J h2)] for h = h1 + H1 h2 (else Y[j + J h])
 };
 
 // round to the nearest tf32 (ties away from zero); the result has its 13 low mantissa bits clear
@@ -305,18 +306,31 @@ __global__ void __launch_bounds__(kT0Threads, 1)
           aph ^= 1;
         }
       }
-      __syncwarp();  // the previous tile's copy-out of the staging rows is done
-      const uint32_t wrow = wsa + lane * static_cast<uint32_t>(J) * 4u;
-#pragma unroll
-      for (int j = 0; j < kT0MaxJ; ++j)
-        if (j < J) t0_sts(wrow + 4u * j, acc[j]);
-      __syncwarp();
       const int64_t h0 = t * kT0Rows + 32 * q;
-      const int64_t nr = min(static_cast<int64_t>(32), p.H - h0);
-      if (nr > 0) {
-        float* out = p.Y + static_cast<int64_t>(J) * h0;
-        const int n = static_cast<int>(nr) * J;
-        for (int e = static_cast<int>(lane); e < n; e += 32) out[e] = t0_lds(wsa + 4u * e);
+      if (p.H1 > 0) {
+        // permuted output Y[h1 + H1 (j + J h2)], h = h1 + H1 h2: for each j the warp's 32 consecutive rows are
+        // (up to an h2 wrap) 32 consecutive floats, stored straight from the registers
+        const int64_t h = h0 + lane;
+        if (h < p.H) {
+          const int64_t h2 = h / p.H1, h1 = h - h2 * p.H1;
+          float* out = p.Y + h1 + p.H1 * static_cast<int64_t>(J) * h2;
+#pragma unroll
+          for (int j = 0; j < kT0MaxJ; ++j)
+            if (j < J) out[p.H1 * j] = acc[j];
+        }
+      } else {
+        __syncwarp();  // the previous tile's copy-out of the staging rows is done
+        const uint32_t wrow = wsa + lane * static_cast<uint32_t>(J) * 4u;
+#pragma unroll
+        for (int j = 0; j < kT0MaxJ; ++j)
+          if (j < J) t0_sts(wrow + 4u * j, acc[j]);
+        __syncwarp();
+        const int64_t nr = min(static_cast<int64_t>(32), p.H - h0);
+        if (nr > 0) {
+          float* out = p.Y + static_cast<int64_t>(J) * h0;
+          const int n = static_cast<int>(nr) * J;
+          for (int e = static_cast<int>(lane); e < n; e += 32) out[e] = t0_lds(wsa + 4u * e);
+        }
       }
     }
   }
@@ -342,7 +356,7 @@ size_t ttm0_tc_ws_bytes(int64_t I, int J) {
 }
 
 int ttm0_tc(const float* X, int64_t I, int64_t H, const float* A, int J, int64_t sj, int64_t si, float* Y, Arena& ar,
-            cudaStream_t s) {
+            cudaStream_t s, int64_t H1) {
   if (!ttm0_tc_ok(X, I, H, J)) {
     set_error("ttm0_tc: unsupported shape or device (I=%lld H=%lld J=%d)", static_cast<long long>(I),
               static_cast<long long>(H), J);
@@ -365,6 +379,7 @@ int ttm0_tc(const float* X, int64_t I, int64_t H, const float* A, int J, int64_t
   }
   p.Bimg = img;
   p.Y = Y;
+  p.H1 = (H1 > 0 && H % H1 == 0) ? H1 : 0;
   // shared memory: stages of (X box 16 KB + B image), the epilogue staging, barriers; ~200 KB
   const uint32_t stage = kT0Rows * 128 + p.b_bytes;
   const uint32_t stg_bytes = 4 * 32 * kT0MaxJ * 4;
