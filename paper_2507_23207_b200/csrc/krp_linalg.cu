@@ -550,14 +550,17 @@ MGPlan plan_mode_gram(const Dims& g, int n) {
 }
 
 // ------------------------------------------------------------------ symmetric eigensolver (Jacobi)
-// One-sided (Hestenes) cyclic Jacobi on the symmetric PSD Gram matrix H: right rotations A <- A J, V <- V J
-// (A = H initially) until the columns of A = H V are mutually orthogonal; then H V = V Λ, so the columns
-// of V are the eigenvectors and ||a_i|| = λ_i.  Round-robin pairing (m-1 rounds of m/2 disjoint pairs per
+// One-sided (Hestenes) cyclic Jacobi on the symmetric PSD Gram matrix H: right rotations A <- A J (A = H
+// initially) until the columns of A = H V are mutually orthogonal; then H V = V Λ, so ||a_i|| = λ_i and
+// v_i = a_i / λ_i: V itself is never formed (the rounds are bound by shared-memory traffic, which this
+// halves).  Round-robin pairing (m-1 rounds of m/2 disjoint pairs per
 // sweep, tabulated in shared memory once); ONE HALF-WARP PER PAIR: 16 lanes hold columns p, q of A and V
 // (rows l, l+16, l+32, l+48 per lane: each half-warp access is one conflict-free 128-byte wavefront),
-// form α = a_p·a_p, β = a_q·a_q, γ = a_p·a_q by xor-butterfly reductions (all 16 lanes end with
-// bit-identical sums, so they form the same rotation), rotate, and write the columns back in place (a
-// round's pairs are disjoint: no double buffer).  One named barrier per round.  The round is issue-bound
+// form γ = a_p·a_q by an xor-butterfly reduction (all 16 lanes end with bit-identical sums, so they form
+// the same rotation) and take α = ||a_p||^2, β = ||a_q||^2 from norms kept in shared memory (recomputed
+// exactly at every sweep start, updated by α' = c²α - 2csγ + s²β, β' = s²α + 2csγ + c²β after a rotation),
+// rotate, and write the columns back in place (a round's pairs are disjoint: no double buffer).  One named
+// barrier per round.  The round is issue-bound
 // (the SM runs m/4 warps of ~160 instructions each), so the rotation uses fast fp32 approximations for the
 // ANGLE only; (c, s) are renormalised in fp64 (c^2 + s^2 = 1 to fp64 rounding), so every update is an
 // exact-to-rounding orthogonal rotation and V stays orthogonal; an approximate angle leaves γ' ~ 1e-6 γ,
@@ -579,19 +582,23 @@ __device__ __forceinline__ void jacobi_pair(int round, int k, int m, int& p, int
 // (c, s) of the rotation orthogonalising columns with Gram [[α, γ], [γ, β]]: t = sign(x) y / (|x| +
 // sqrt(x^2 + y^2)) with x = β - α, y = 2γ (sign(0) = +1), c = 1 / sqrt(1 + t^2), s = t c; the pair is
 // then a_p' = c a_p - s a_q, a_q' = s a_p + c a_q.
+__device__ __forceinline__ double rsqrt_approx_f64(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return r;
+}
+__device__ __forceinline__ double rcp_approx_f64(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return r;
+}
 __device__ __forceinline__ void jacobi_rot(double alpha, double beta, double gamma, double& c, double& s) {
-  double x = beta - alpha, y = 2.0 * gamma;
-  // scale by a power of two so that the larger of |x|, |y| is in [1, 2): no fp32 overflow / underflow
-  const double mx = fmax(fabs(x), fabs(y));
-  const int e = static_cast<int>((__double_as_longlong(mx) >> 52) & 0x7FF) - 1023;
-  const double sc = __longlong_as_double(static_cast<long long>(1023 - e) << 52);
-  x *= sc;
-  y *= sc;
-  const float xf = static_cast<float>(x), yf = static_cast<float>(y);
-  const float r2 = fmaf(xf, xf, yf * yf);
-  const float tf = __fdividef(xf >= 0.f ? yf : -yf, fabsf(xf) + r2 * rsqrtf(r2));
-  const float cf = rsqrtf(fmaf(tf, tf, 1.f));
-  double cd = static_cast<double>(cf), sd = static_cast<double>(tf * cf);
+  const double x = beta - alpha, y = 2.0 * gamma;
+  // the angle from the hardware's approximate fp64 reciprocal / reciprocal square root (~20 bits; full fp64
+  // range, so no scaling is needed)
+  const double r2 = fma(x, x, y * y);
+  const double t = (x >= 0.0 ? y : -y) * rcp_approx_f64(fabs(x) + r2 * rsqrt_approx_f64(r2));
+  double cd = rsqrt_approx_f64(fma(t, t, 1.0)), sd = t * cd;
   // two Newton steps for 1/sqrt(n), n = c^2 + s^2 = 1 + O(1e-6): |c^2 + s^2 - 1| -> O(1e-16)
 #pragma unroll
   for (int it = 0; it < 2; ++it) {
@@ -632,6 +639,7 @@ __global__ void __launch_bounds__(1024) jacobi_top_kernel(EigBatch batch, int J)
   double* V = dyn_smem + 64 * 64;        // [64][64]
   __shared__ uint16_t ptab[kGramMaxR - 1][kGramMaxR / 2];  // round-robin pairs: p | q << 8
   __shared__ double lam[kGramMaxR];
+  __shared__ double cn[kGramMaxR];  // ||a_j||^2: exact at each sweep start, updated by the rotation formulas
   __shared__ int order[kGramMaxR];
   __shared__ int rotated[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -646,7 +654,6 @@ __global__ void __launch_bounds__(1024) jacobi_top_kernel(EigBatch batch, int J)
   for (int e = tid; e < 64 * 64; e += blockDim.x) {
     const int j = e >> 6, i = e & 63;
     A[e] = (i < J && j < J) ? Hm[i * J + j] : 0.0;  // H symmetric: column j = row j
-    V[e] = (i == j) ? 1.0 : 0.0;
   }
   if (tid < 2) rotated[tid] = 0;
   __syncthreads();
@@ -654,16 +661,27 @@ __global__ void __launch_bounds__(1024) jacobi_top_kernel(EigBatch batch, int J)
   const int l = lane & 15;
 #ifdef KRP_DEV_TRACE
   int dev_sweeps = 0;
+  long long dv_t0 = clock64(), dv_red = 0, dv_rot = 0, dv_bar = 0, dv_rounds = 0;
 #endif
   for (int sweep = 0; sweep < 30 && m >= 2; ++sweep) {
 #ifdef KRP_DEV_TRACE
     dev_sweeps = sweep + 1;
 #endif
     const int flag = sweep & 1;  // rotated[flag] collects this sweep; rotated[flag ^ 1] is reset for the next
+    for (int j = warp; j < m; j += blockDim.x >> 5) {  // exact column norms (fixed-order warp sums)
+      const double a0 = A[j * 64 + lane], a1 = A[j * 64 + lane + 32];
+      const double n2 = warp_sum_f64(fma(a0, a0, a1 * a1));
+      if (lane == 0) cn[j] = n2;
+    }
+    __syncthreads();
     if (warp < nwork) {
+      const bool act = k < half;
+      int pq = act ? ptab[0][k] : 0;
+      double vc = 1.0, vs = 0.0;
       for (int round = 0; round < m - 1; ++round) {
-        const bool act = k < half;
-        const int pq = act ? ptab[round][k] : 0;
+#ifdef KRP_DEV_TRACE
+        const long long c0 = clock64();
+#endif
         double* ap = A + (pq & 0xFF) * 64 + l;
         double* aq = A + (pq >> 8) * 64 + l;
         double pv[4], qv[4];
@@ -672,36 +690,44 @@ __global__ void __launch_bounds__(1024) jacobi_top_kernel(EigBatch batch, int J)
           pv[t] = act ? ap[16 * t] : 0.0;
           qv[t] = act ? aq[16 * t] : 0.0;
         }
-        double al = 0.0, be = 0.0, ga = 0.0;
+        // α, β: the tracked column norms (a sweep without rotations keeps them exact, so the stopping test is
+        // exact); γ: a 16-lane butterfly
+        const double al = act ? cn[pq & 0xFF] : 0.0, be = act ? cn[pq >> 8] : 0.0;
+        double ga = 0.0;
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          al = fma(pv[t], pv[t], al);
-          be = fma(qv[t], qv[t], be);
-          ga = fma(pv[t], qv[t], ga);
-        }
-        al = halfwarp_sum_f64(al);
-        be = halfwarp_sum_f64(be);
+        for (int t = 0; t < 4; ++t) ga = fma(pv[t], qv[t], ga);
         ga = halfwarp_sum_f64(ga);
+#ifdef KRP_DEV_TRACE
+        const long long c1 = clock64();
+#endif
         if (act && ga * ga > 1e-26 * (al * be)) {  // uniform within the half-warp
-          double c, sn;
-          jacobi_rot(al, be, ga, c, sn);
+          jacobi_rot(al, be, ga, vc, vs);
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
-            ap[16 * t] = c * pv[t] - sn * qv[t];
-            aq[16 * t] = sn * pv[t] + c * qv[t];
+            ap[16 * t] = vc * pv[t] - vs * qv[t];
+            aq[16 * t] = vs * pv[t] + vc * qv[t];
           }
-          double* vp = V + (pq & 0xFF) * 64 + l;
-          double* vq = V + (pq >> 8) * 64 + l;
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const double v0 = vp[16 * t], w0 = vq[16 * t];
-            vp[16 * t] = c * v0 - sn * w0;
-            vq[16 * t] = sn * v0 + c * w0;
+          if (l == 0) {
+            rotated[flag] = 1;
+            const double cc = vc * vc, ss = vs * vs, cs2 = 2.0 * vc * vs * ga;
+            cn[pq & 0xFF] = fma(cc, al, fma(ss, be, -cs2));
+            cn[pq >> 8] = fma(ss, al, fma(cc, be, cs2));
           }
-          if (l == 0) rotated[flag] = 1;
         }
+        const int next = (act && round + 1 < m - 1) ? ptab[round + 1][k] : 0;
         // all pairs of this round are done before the next round re-pairs the columns
+#ifdef KRP_DEV_TRACE
+        const long long c2 = clock64();
+#endif
         asm volatile("bar.sync 1, %0;" ::"r"(nwork * 32) : "memory");
+#ifdef KRP_DEV_TRACE
+        const long long c3 = clock64();
+        dv_red += c1 - c0;
+        dv_rot += c2 - c1;
+        dv_bar += c3 - c2;
+        ++dv_rounds;
+#endif
+        pq = next;
       }
     }
     __syncthreads();
@@ -711,7 +737,10 @@ __global__ void __launch_bounds__(1024) jacobi_top_kernel(EigBatch batch, int J)
     if (!again) break;
   }
 #ifdef KRP_DEV_TRACE
-  if (tid == 0) printf("jacobi block %d J=%d: %d sweeps\n", blockIdx.x, J, dev_sweeps);
+  if (tid == 0)
+    printf("jacobi block %d J=%d: %d sweeps, %lld rounds, %lld cycles total; per round: red %lld rot %lld bar %lld\n",
+           blockIdx.x, J, dev_sweeps, dv_rounds, clock64() - dv_t0, dv_red / max(dv_rounds, 1LL),
+           dv_rot / max(dv_rounds, 1LL), dv_bar / max(dv_rounds, 1LL));
 #endif
   // λ_j = ||a_j|| (fixed-order warp sums), then the r largest, descending
   for (int j = warp; j < J; j += blockDim.x >> 5) {
@@ -732,18 +761,53 @@ __global__ void __launch_bounds__(1024) jacobi_top_kernel(EigBatch batch, int J)
     }
   }
   __syncthreads();
+  // eigenvectors v_t = a_t / λ_t (H V = V Λ); a numerically null λ (<= 64 u λ_max: its column carries no
+  // direction) gets a unit vector orthogonalised against the others instead (serial; rare: r > rank H)
+  double* Uf = V;  // [r][64]
+  const double thr = 64.0 * 1.1102230246251565e-16 * lam[order[0]];
+  for (int e = tid; e < r * 64; e += blockDim.x) {
+    const int t = e >> 6, i = e & 63;
+    const double lt = lam[order[t]];
+    Uf[e] = (i < J && lt > thr) ? A[order[t] * 64 + i] / lt : 0.0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int t = 0; t < r; ++t) {
+      if (lam[order[t]] > thr) continue;
+      for (int j = 0; j < J; ++j) {
+        double* v = Uf + t * 64;
+        for (int i = 0; i < J; ++i) v[i] = (i == j) ? 1.0 : 0.0;
+        for (int pass = 0; pass < 2; ++pass)
+          for (int u = 0; u < r; ++u) {
+            if (u == t) continue;
+            const double* w = Uf + u * 64;
+            double dp = 0.0;
+            for (int i = 0; i < J; ++i) dp = fma(w[i], v[i], dp);
+            for (int i = 0; i < J; ++i) v[i] = fma(-dp, w[i], v[i]);
+          }
+        double nn = 0.0;
+        for (int i = 0; i < J; ++i) nn = fma(v[i], v[i], nn);
+        if (nn > 0.25) {
+          const double inv = 1.0 / sqrt(nn);
+          for (int i = 0; i < J; ++i) v[i] *= inv;
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
   // canonical signs (reading R24): each eigenvector's entry of largest magnitude (first on ties) positive
   for (int t = tid; t < r; t += blockDim.x) {
-    const double* v = V + order[t] * 64;
+    const double* v = Uf + t * 64;
     int best = 0;
     for (int i = 1; i < J; ++i)
       if (fabs(v[i]) > fabs(v[best])) best = i;
-    lam[t] = v[best] < 0.0 ? -1.0 : 1.0;  // lam is free again: reused for the signs
+    lam[t] = v[best] < 0.0 ? -1.0 : 1.0;  // lam (read above) is reused for the signs
   }
   __syncthreads();
   for (int e = tid; e < J * r; e += blockDim.x) {
     const int i = e / r, t = e % r;
-    U[e] = static_cast<float>(lam[t] * V[order[t] * 64 + i]);
+    U[e] = static_cast<float>(lam[t] * Uf[t * 64 + i]);
   }
 }
 

@@ -410,3 +410,17 @@ def test_hadamard_tucker_vs_oracle(krp):
         assert abs(e - e_ref) <= ERR_TOL, (ls, e, e_ref)
         if ls == ranks:
             assert e < 1e-5, e
+
+
+def test_rhosvd_ranks_above_the_multilinear_rank(krp):
+    """r_n > rank of the core's unfoldings: the truncation eigenproblem has (numerically) null eigenvalues;
+    the factors must still be orthonormal and the exact tensor recovered."""
+    dims, R, ranks = (24, 20, 16), 8, (5, 5, 5)
+    core = np.random.default_rng(2).standard_normal((2, 2, 2))
+    us = [np.linalg.qr(np.random.default_rng(10 + k).standard_normal((n, 2)))[0] for k, n in enumerate(dims)]
+    x = oracle.multi_ttm(core, us).reshape(-1, order="F").astype(np.float32)
+    om = [_dev(o) for o in synth.omegas(dims, R, 3)]
+    Q, g, err = krp.krp_rhosvd(_dev(x), dims, ranks, om, with_error=True)
+    _check_factors(Q, ranks)
+    assert np.isfinite(g.cpu().numpy()).all()
+    assert err <= 1e-6, err
