@@ -75,55 +75,78 @@ __global__ void sum_partials_f64_kernel(const double* __restrict__ partial, int 
 // a breakdown that cannot be shifted sets flag |= 2.
 // allow_shift == 2: the third (refinement) pass — factorise only if the first pass was shifted
 // (flag & 1), else write Linv = I so that the pass is an exact copy (plain CholeskyQR2).
-__global__ void __launch_bounds__(256) chol_inv_kernel(const double* __restrict__ G, int R, int64_t rows,
-                                                       double* __restrict__ Linv_out, int* flag, int allow_shift) {
+__device__ __forceinline__ double rcp_nr_f64(double x) {  // 1 / x: hardware approximation + 2 Newton steps
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = r * fma(-x, r, 2.0);
+  return r * fma(-x, r, 2.0);
+}
+
+// Register-resident right-looking Cholesky and triangular inverse, 1024 threads, ONE barrier per step:
+// thread t owns the lower-triangle entries e = t, t + 1024, t + 2048 (e = i(i+1)/2 + k, k <= i) in
+// registers.  Cholesky step j: column j (unscaled) is final, broadcast through a double-buffered shared
+// column (its owners wrote it while finishing step j-1); each owner of (i, k), k > j, subtracts
+// a_ij a_kj / a_jj and, if k == j+1, publishes the result for step j+1.  Column scalings L_ij = a_ij /
+// sqrt(a_jj) are applied once at the end.  Inverse: rows of U = unscaled L^-1 likewise (step i broadcasts
+// row i; U_rc -= (L_ri / L_ii) U_ic), scaled by 1 / L_ii at the end.
+constexpr int kCholThreads = 1024, kCholSlots = 3;  // 3 x 1024 >= 64 * 65 / 2
+__global__ void __launch_bounds__(kCholThreads) chol_inv_kernel(const double* __restrict__ G, int R, int64_t rows,
+                                                                double* __restrict__ Linv_out, int* flag,
+                                                                int allow_shift) {
   if (allow_shift == 2 && !(*flag & 1)) {
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) Linv_out[e] = (e / R == e % R) ? 1.0 : 0.0;
     return;
   }
   if (allow_shift == 2) allow_shift = 0;
-  extern __shared__ double dyn_smem[];
-  double(*A)[kGramMaxR + 1] = reinterpret_cast<double(*)[kGramMaxR + 1]>(dyn_smem);
-  double(*Li)[kGramMaxR + 1] = reinterpret_cast<double(*)[kGramMaxR + 1]>(dyn_smem + kGramMaxR * (kGramMaxR + 1));
-  __shared__ int fail;
+  __shared__ double colb[2][kGramMaxR];   // Cholesky: broadcast column; inverse: broadcast row
+  __shared__ double Ls[kGramMaxR][kGramMaxR + 1];
+  __shared__ double rdiag[kGramMaxR];     // 1 / L_jj
   __shared__ double shift;
-  __shared__ double rdiag[kGramMaxR];  // 1 / L[j][j]
-  const int tid = threadIdx.x, nt = blockDim.x;  // 256 threads: a 16 x 16 grid for the rank-1 updates
-  const int tx = tid & 15, ty = tid >> 4;
+  const int tid = threadIdx.x;
+  const int ne = R * (R + 1) / 2;
+  int ei[kCholSlots], ek[kCholSlots];
+#pragma unroll
+  for (int u = 0; u < kCholSlots; ++u) {
+    const int e = tid + u * kCholThreads;
+    int i = static_cast<int>((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+    while (i * (i + 1) / 2 > e) --i;
+    while ((i + 1) * (i + 2) / 2 <= e) ++i;
+    ei[u] = e < ne ? i : -1;
+    ek[u] = e < ne ? e - i * (i + 1) / 2 : -1;
+  }
   if (tid == 0) shift = 0.0;
+  bool failed = false;
+  double a[kCholSlots];
   for (int attempt = 0; attempt < 2; ++attempt) {
     __syncthreads();
-    for (int e = tid; e < R * R; e += nt) {
-      const int i = e / R, j = e % R;
-      A[i][j] = G[e] + (i == j ? shift : 0.0);
+#pragma unroll
+    for (int u = 0; u < kCholSlots; ++u) {
+      a[u] = ei[u] >= 0 ? G[ei[u] * R + ek[u]] + (ei[u] == ek[u] ? shift : 0.0) : 0.0;
+      if (ek[u] == 0) colb[0][ei[u]] = a[u];
     }
-    if (tid == 0) fail = 0;
     __syncthreads();
-    // right-looking Cholesky on the lower triangle: column j is final once the updates of columns < j
-    // have been applied; each step is a pivot, a column scale and a rank-1 trailing update
+    failed = false;
     for (int j = 0; j < R; ++j) {
-      const double dgl = A[j][j];
-      if (!(dgl > 0.0) || !isfinite(dgl)) {  // every thread reads the same value: a uniform exit
-        if (tid == 0) fail = 1;
+      const double* col = colb[j & 1];
+      double* nxt = colb[(j + 1) & 1];
+      const double dgl = col[j];
+      if (!(dgl > 0.0) || !isfinite(dgl)) {  // every thread reads the same pivot: a uniform exit
+        failed = true;
         break;
       }
-      const double rl = rsqrt(dgl);  // 1 / L[j][j]: one reciprocal square root instead of sqrt + divides
-      __syncthreads();  // all threads have read A[j][j]
-      for (int i = j + 1 + tid; i < R; i += nt) A[i][j] *= rl;
-      if (tid == 0) {
-        A[j][j] = dgl * rl;  // L[j][j] = sqrt(dgl)
-        rdiag[j] = rl;
-      }
-      __syncthreads();
-      // trailing (i, k), j < k <= i < R, on a 16 x 16 thread grid (no integer division)
-      for (int i = j + 1 + ty; i < R; i += 16) {
-        const double lij = A[i][j];
-        for (int k = j + 1 + tx; k <= i; k += 16) A[i][k] -= lij * A[k][j];
+      const double rinv = rcp_nr_f64(dgl);
+      if (tid == 0) rdiag[j] = rsqrt(dgl);
+#pragma unroll
+      for (int u = 0; u < kCholSlots; ++u) {
+        const int i = ei[u], k = ek[u];
+        if (k > j) {
+          a[u] = fma(-col[i] * rinv, col[k], a[u]);
+          if (k == j + 1) nxt[i] = a[u];
+        }
       }
       __syncthreads();
     }
-    __syncthreads();
-    if (!fail) break;
+    if (!failed) break;
     if (!allow_shift || attempt == 1) {
       if (tid == 0) atomicOr(flag, 2);
       break;
@@ -136,25 +159,40 @@ __global__ void __launch_bounds__(256) chol_inv_kernel(const double* __restrict_
     }
   }
   __syncthreads();
-  if (fail) {
-    for (int e = tid; e < R * R; e += nt) Linv_out[e] = 0.0;
+  if (failed) {
+    for (int e = tid; e < R * R; e += blockDim.x) Linv_out[e] = 0.0;
     return;
   }
-  // L^{-1} by row-oriented forward elimination applied to the identity, all columns at once:
-  // row i is final after dividing by L[i][i]; it is then eliminated from the rows below it
-  for (int e = tid; e < R * R; e += nt) Li[e / R][e % R] = (e / R == e % R) ? 1.0 : 0.0;
+  // L = scaled columns, into shared memory for the inverse
+#pragma unroll
+  for (int u = 0; u < kCholSlots; ++u)
+    if (ei[u] >= 0) Ls[ei[u]][ek[u]] = a[u] * rdiag[ek[u]];
+  // U = identity (unscaled inverse), row 0 published
+#pragma unroll
+  for (int u = 0; u < kCholSlots; ++u) {
+    a[u] = (ei[u] >= 0 && ei[u] == ek[u]) ? 1.0 : 0.0;
+    if (ei[u] == 0) colb[0][ek[u]] = a[u];
+  }
   __syncthreads();
   for (int i = 0; i < R; ++i) {
+    const double* row = colb[i & 1];
+    double* nxt = colb[(i + 1) & 1];
     const double rd = rdiag[i];
-    for (int c = tid; c <= i; c += nt) Li[i][c] *= rd;
-    __syncthreads();
-    for (int r = i + 1 + ty; r < R; r += 16) {  // rows i+1..R-1, columns 0..i
-      const double lri = A[r][i];
-      for (int c = tx; c <= i; c += 16) Li[r][c] -= lri * Li[i][c];
+#pragma unroll
+    for (int u = 0; u < kCholSlots; ++u) {
+      const int r = ei[u], c = ek[u];
+      if (r > i && c <= i) a[u] = fma(-Ls[r][i] * rd, row[c], a[u]);
+      if (r == i + 1) nxt[c] = a[u];
     }
     __syncthreads();
   }
-  for (int e = tid; e < R * R; e += nt) Linv_out[e] = Li[e / R][e % R];
+  for (int e = tid; e < R * R; e += blockDim.x) {
+    const int i = e / R, c = e % R;
+    if (c > i) Linv_out[e] = 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < kCholSlots; ++u)
+    if (ei[u] >= 0) Linv_out[ei[u] * R + ek[u]] = a[u] * rdiag[ei[u]];
 }
 
 // Q[i][a] = sum_{b <= a} Y[i][b] * Linv[a][b]
@@ -894,20 +932,20 @@ int cholqr(const float* Y, int64_t rows, int R, float* Qf, double* Qd, int* flag
   const unsigned nb = static_cast<unsigned>((tot + 255) / 256);
   // pass 1 (shift allowed)
   KRP_TRY(gram<float>(Y, rows, R, G, part, s));
-  chol_inv_kernel<<<1, 256, kSquareSmem, s>>>(G, R, rows, Li, flag_dev, 1);
+  chol_inv_kernel<<<1, kCholThreads, 0, s>>>(G, R, rows, Li, flag_dev, 1);
   KRP_CHECK_LAUNCH();
   apply_linv_kernel<float><<<nb, 256, 0, s>>>(Y, rows, R, Li, Q1, nullptr);
   KRP_CHECK_LAUNCH();
   // pass 2
   KRP_TRY(gram<double>(Q1, rows, R, G, part, s));
-  chol_inv_kernel<<<1, 256, kSquareSmem, s>>>(G, R, rows, Li, flag_dev, 0);
+  chol_inv_kernel<<<1, kCholThreads, 0, s>>>(G, R, rows, Li, flag_dev, 0);
   KRP_CHECK_LAUNCH();
   apply_linv_kernel<double><<<nb, 256, 0, s>>>(Q1, rows, R, Li, Q2, nullptr);
   KRP_CHECK_LAUNCH();
   // pass 3 (restores orthogonality after a shifted first pass; skipped on the device otherwise, so the
   // unshifted case is plain CholeskyQR2 and the last apply is an exact copy through Linv = I)
   KRP_TRY(gram<double>(Q2, rows, R, G, part, s, flag_dev));
-  chol_inv_kernel<<<1, 256, kSquareSmem, s>>>(G, R, rows, Li, flag_dev, 2);
+  chol_inv_kernel<<<1, kCholThreads, 0, s>>>(G, R, rows, Li, flag_dev, 2);
   KRP_CHECK_LAUNCH();
   apply_linv_kernel<double><<<nb, 256, 0, s>>>(Q2, rows, R, Li, Qd, Qf);
   KRP_CHECK_LAUNCH();
