@@ -35,6 +35,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "krp_common.cuh"
 #include "krp_internal.h"
@@ -58,6 +59,7 @@ struct Ttm0Params {
   int64_t T;         // tiles = ceil(H / 128)
   int NS;            // smem stages (X box + B image)
   int NC;            // TMEM chunk slots
+  int kpd;           // K chunks accumulated in TMEM per drain (1: the accuracy design; > 1 development A/B)
   uint32_t sm_x, sm_b, sm_stg, sm_bar;
   uint32_t b_bytes;  // one B image chunk: 2 Np rows x 128 B
   const float* Bimg; // [nk][2 Np][32] swizzled: rows [0, Np) A_hi, [Np, 2Np) A_lo
@@ -106,6 +108,9 @@ __device__ __forceinline__ float t0_lds(uint32_t saddr) {
 }
 
 #define T0WAIT(bar, par) mbar_wait_hint((bar), (par), 10000000u)
+#ifndef KRP_T0_DBG
+#define KRP_T0_DBG 0  // development probes (results garbage): 1 epilogue skips TMEM, 2 split skips smem/ALU, 4 no MMAs
+#endif
 
 __global__ void __launch_bounds__(kT0Threads, 1)
     ttm0_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Ttm0Params p) {
@@ -181,7 +186,8 @@ __global__ void __launch_bounds__(kT0Threads, 1)
     uint32_t ph = 0, cph = 0, aph = 0;
     for (int64_t t = t0; t < t1; ++t) {
       for (int kc = 0; kc < nk; ++kc) {
-        T0WAIT(&acc_empty[as], aph ^ 1);
+        const bool first = kc % p.kpd == 0, last = kc % p.kpd == p.kpd - 1 || kc == nk - 1;
+        if (first) T0WAIT(&acc_empty[as], aph ^ 1);
         T0WAIT(&full[st], ph);
         T0WAIT(&lo_full[cs], cph);
         tc_fence_after();
@@ -190,13 +196,13 @@ __global__ void __launch_bounds__(kT0Threads, 1)
         const uint32_t thi = tbase + tm_slot + static_cast<uint32_t>(cs * kT0SlotCols);
         if (leader) {
 #pragma unroll
-          for (int ks = 0; ks < kT0K / 8; ++ks) {  // K = 8 per MMA: +32 B on the B descriptor's start address
-            mma_tf32_ts(d1, thi + 8 * ks, bd + ks * 2, idesc_cat, ks ? 1u : 0u);       // hi x [A_hi | A_lo]
+          for (int ks = 0; ks < kT0K / 8 && !(KRP_T0_DBG & 4); ++ks) {  // K = 8 per MMA: +32 B on the B descriptor's start address
+            mma_tf32_ts(d1, thi + 8 * ks, bd + ks * 2, idesc_cat, (ks || !first) ? 1u : 0u);  // hi x [A_hi | A_lo]
             mma_tf32_ts(d2, thi + 32 + 8 * ks, bd + ks * 2, idesc_lo, 1u);             // lo x A_hi
           }
           mma_commit(&empty[st]);
           mma_commit(&lo_free[cs]);
-          mma_commit(&acc_full[as]);
+          if (last) mma_commit(&acc_full[as]);
         }
         __syncwarp();
         if (++st == p.NS) {
@@ -207,7 +213,7 @@ __global__ void __launch_bounds__(kT0Threads, 1)
           cs = 0;
           cph ^= 1;
         }
-        if (++as == kT0NA) {
+        if (last && ++as == kT0NA) {
           as = 0;
           aph ^= 1;
         }
@@ -229,7 +235,7 @@ __global__ void __launch_bounds__(kT0Threads, 1)
         const uint32_t rowa = smem_u32(xs) + static_cast<uint32_t>(st) * (kT0Rows * 128) + row * 128u;
         uint32_t v[kT0K];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
+        for (int c = 0; c < 8 * !(KRP_T0_DBG & 2); ++c) {
           float a0, a1, a2, a3;
           lds_v4(rowa + ((static_cast<uint32_t>(c) ^ rx) << 4), a0, a1, a2, a3);
           v[4 * c] = __float_as_uint(a0), v[4 * c + 1] = __float_as_uint(a1);
@@ -277,13 +283,13 @@ __global__ void __launch_bounds__(kT0Threads, 1)
       float acc[kT0MaxJ];
 #pragma unroll
       for (int j = 0; j < kT0MaxJ; ++j) acc[j] = 0.f;
-      for (int kc = 0; kc < nk; ++kc) {
+      for (int kc = 0; kc < nk; kc += p.kpd) {
         T0WAIT(&acc_full[as], aph);
         tc_fence_after();
         const uint32_t d1 = tbase + lane_off + static_cast<uint32_t>(as * 2 * Np);
 #pragma unroll
         for (int c = 0; c < kT0MaxJ; c += 16) {
-          if (c < Np) {
+          if (c < Np && !(KRP_T0_DBG & 1)) {
             uint32_t hh[16], hl[16];
             tmem_ld<16>(d1 + c, hh);
             tmem_ld<16>(d1 + Np + c, hl);
@@ -391,6 +397,8 @@ int ttm0_tc(const float* X, int64_t I, int64_t H, const float* A, int J, int64_t
   p.sm_bar = p.sm_stg + stg_bytes;
   const uint32_t smem_bytes = p.sm_bar + (2 * p.NS + 2 * kT0MaxNC + 2 * kT0NA) * 8 + 16 + 1024;
   p.NC = std::min(kT0MaxNC, (512 - kT0NA * 2 * p.Np) / kT0SlotCols);  // TMEM: 2 x 2 Np + NC x 64 <= 512
+  p.kpd = 1;
+  if (const char* e = getenv("KRP_T0_KPD")) p.kpd = std::max(1, atoi(e));  // development A/B only
 
   CUtensorMap tmap;
   {
