@@ -60,13 +60,35 @@ __global__ void __launch_bounds__(256) gram_partial_kernel(const T* __restrict__
 }
 
 // gate (optional): run only if *gate & 1 (the shifted first CholeskyQR pass happened)
-__global__ void sum_partials_f64_kernel(const double* __restrict__ partial, int P, int64_t len,
-                                        double* __restrict__ out, const int* __restrict__ gate = nullptr) {
-  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= len || (gate && !(*gate & 1))) return;
-  double s = 0.0;
-  for (int p = 0; p < P; ++p) s += partial[static_cast<int64_t>(p) * len + idx];
-  out[idx] = s;
+// out[idx] = sum_p partial[p * len + idx] in a fixed order: warp w of the block sums p = w, w+32, ... for
+// 32 consecutive idx (coalesced; four independent chains so four loads are in flight), and warp 0 adds the
+// 32 warp sums in order w = 0..31.  Launch: ceil(len/32) blocks of 1024 threads.
+__global__ void __launch_bounds__(1024) sum_partials_f64_kernel(const double* __restrict__ partial, int P,
+                                                                int64_t len, double* __restrict__ out,
+                                                                const int* __restrict__ gate = nullptr) {
+  __shared__ double ws[32][33];
+  if (gate && !(*gate & 1)) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * 32 + lane;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  if (idx < len) {
+    const double* src = partial + idx;
+    int p = w;
+    for (; p + 96 < P; p += 128) {
+      s0 += src[static_cast<int64_t>(p) * len];
+      s1 += src[static_cast<int64_t>(p + 32) * len];
+      s2 += src[static_cast<int64_t>(p + 64) * len];
+      s3 += src[static_cast<int64_t>(p + 96) * len];
+    }
+    for (; p < P; p += 32) s0 += src[static_cast<int64_t>(p) * len];
+  }
+  ws[w][lane] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  if (w == 0 && idx < len) {
+    double t = 0.0;
+    for (int k = 0; k < 32; ++k) t += ws[k][lane];
+    out[idx] = t;
+  }
 }
 
 // ------------------------------------------------------------------ Cholesky + triangular inverse
@@ -244,7 +266,7 @@ int gram(const T* Y, int64_t rows, int R, double* G, double* partial, cudaStream
   gram_partial_kernel<T><<<gp.P, 256, 0, s>>>(Y, rows, R, gp.rows_per_block, partial, gate);
   KRP_CHECK_LAUNCH();
   const int64_t len = static_cast<int64_t>(R) * R;
-  sum_partials_f64_kernel<<<static_cast<unsigned>((len + 255) / 256), 256, 0, s>>>(partial, gp.P, len, G, gate);
+  sum_partials_f64_kernel<<<static_cast<unsigned>((len + 31) / 32), 1024, 0, s>>>(partial, gp.P, len, G, gate);
   KRP_CHECK_LAUNCH();
   return KRP_OK;
 }
@@ -488,23 +510,28 @@ int launch_ttm_mode0q(const float* X, int64_t I, int64_t H, const float* A, int 
 // ------------------------------------------------------------------ mode-n Gram
 // H[a][b] = sum over fibers f=(l,h) of T[l + L(a + J h)] T[l + L(b + J h)], fp64.
 // Fibers come in chunks of 32, converted to fp64 once into shared memory.  Thread blk of a group owns the
-// 4 x 4 block (a in 4ta.., b in 4tb..) of H: per fiber it reads 4 + 4 doubles (two LDS.128 each; lanes of
-// a warp share ta, so the a-reads broadcast) for 16 DFMAs.  With J <= 44 several groups split each
-// chunk's fibers (fiber ff goes to group ff % G) and are summed in group order at the end, so the
-// result is deterministic for a given plan.
+// 4 x 4 block (a in 4ta.., b in 4tb..) of H, upper block triangle only (ta <= tb; H is symmetric and the
+// lower blocks are mirrored at the end): per fiber it reads 4 + 4 doubles (two LDS.128 each) for 16 DFMAs.
+// Several groups (up to 8) split each chunk's fibers (fiber ff goes to group ff % G) and are summed in
+// group order at the end, so the result is deterministic for a given plan.
 constexpr int kMgPitch = kGramMaxR + 2;  // doubles; 16-byte aligned rows
 __global__ void __launch_bounds__(256) mode_gram_partial_kernel(const float* __restrict__ T, int64_t L, int J,
                                                                 int64_t H, int64_t fibers_per_block,
                                                                 double* __restrict__ partial) {
   __shared__ __align__(16) double F[32][kMgPitch];
-  __shared__ double red[3 * 64 * 16];
+  __shared__ double red[3456];  // (G - 1) * T2 * 16 <= 3456 for every J <= 64
   const int tid = threadIdx.x;
-  const int nblk = (J + 3) >> 2, T2 = nblk * nblk;
+  const int nblk = (J + 3) >> 2, T2 = nblk * (nblk + 1) / 2;
   int G = 256 / T2;
-  G = G < 1 ? 1 : (G > 4 ? 4 : G);
+  G = G < 1 ? 1 : (G > 8 ? 8 : G);
   const int g = tid / T2, blk = tid - g * T2;
   const bool active = g < G;
-  const int ta = blk / nblk, tb = blk - (blk / nblk) * nblk;
+  int ta = 0, tb = blk;  // blk -> (ta, tb), ta <= tb, row-major over the upper block triangle
+  while (tb >= nblk - ta) {
+    tb -= nblk - ta;
+    ++ta;
+  }
+  tb += ta;
   const int Jp = nblk * 4;
   const int64_t nf = L * H;
   const int64_t f_begin = static_cast<int64_t>(blockIdx.x) * fibers_per_block;
@@ -566,7 +593,10 @@ __global__ void __launch_bounds__(256) mode_gram_partial_kernel(const float* __r
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int ra = 4 * ta + i, cb = 4 * tb + j;
-        if (ra < J && cb < J) out[ra * J + cb] = acc[i][j];
+        if (ra < J && cb < J) {
+          out[ra * J + cb] = acc[i][j];
+          out[cb * J + ra] = acc[i][j];
+        }
       }
   }
 }
@@ -799,10 +829,12 @@ __global__ void __launch_bounds__(1024) jacobi_top_kernel(EigBatch batch, int J)
     }
   }
   __syncthreads();
-  // eigenvectors v_t = a_t / λ_t (H V = V Λ); a numerically null λ (<= 64 u λ_max: its column carries no
-  // direction) gets a unit vector orthogonalised against the others instead (serial; rare: r > rank H)
+  // eigenvectors v_t = a_t / λ_t (H V = V Λ).  The converged columns are pairwise orthogonal RELATIVE to
+  // their own norms, however small (noise-level λ included), so a_t / λ_t is orthonormal; only a column
+  // that is exactly zero (or underflows: λ_t <= 1e-150 λ_max; r > rank H) gets a unit vector orthogonalised
+  // against the others instead (serial, rare)
   double* Uf = V;  // [r][64]
-  const double thr = 64.0 * 1.1102230246251565e-16 * lam[order[0]];
+  const double thr = 1e-150 * lam[order[0]];
   for (int e = tid; e < r * 64; e += blockDim.x) {
     const int t = e >> 6, i = e & 63;
     const double lt = lam[order[t]];
@@ -1020,7 +1052,7 @@ int mode_gram(const float* T, const Dims& g, int n, double* H, Arena& ar, cudaSt
   mode_gram_partial_kernel<<<p.P, 256, 0, s>>>(T, L, J, Hh, p.per_block, part);
   KRP_CHECK_LAUNCH();
   const int64_t len = static_cast<int64_t>(J) * J;
-  sum_partials_f64_kernel<<<static_cast<unsigned>((len + 255) / 256), 256, 0, s>>>(part, p.P, len, H);
+  sum_partials_f64_kernel<<<static_cast<unsigned>((len + 31) / 32), 1024, 0, s>>>(part, p.P, len, H);
   KRP_CHECK_LAUNCH();
   ar.off = mark;
   return KRP_OK;

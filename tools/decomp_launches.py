@@ -8,7 +8,7 @@ import paper_2507_23207_b200 as krp
 alg = sys.argv[1]
 name = sys.argv[2] if len(sys.argv) > 2 else ("c5" if alg == "rhosvd" else "c3")
 cfg = synth.config(name)
-x = torch.randn(cfg.N, device="cuda")
+x = torch.from_numpy(synth.tensor(cfg, 0)).cuda()  # the config's own data (spectra drive the eigensolver)
 if alg == "rhosvd":
     om = [torch.from_numpy(o).cuda() for o in synth.omegas(cfg.dims, cfg.R, 0)]
     ws = torch.empty(krp.krp_workspace_bytes(krp.OP_RHOSVD, cfg.dims, cfg.R, cfg.ranks), dtype=torch.uint8, device="cuda")
