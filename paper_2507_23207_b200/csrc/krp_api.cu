@@ -631,6 +631,9 @@ static int sthosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_
       scratch = std::max(scratch, dense ? gaussian_sketch_ws_bytes(cg, i) : sketch_ws_bytes(cg, R, want));
       scratch = std::max(scratch, cholqr_ws_bytes(gd[i], R));
       scratch = std::max(scratch, ttm_ws_bytes(cg, i, R));
+      if (i == 0)  // the fused first step: B = X x_1 Q^T with its mode-1 Gram partials (4 per CTA)
+        scratch = std::max(scratch, ttm_ws_bytes(cg, 0, R) +
+                                        align_up(static_cast<size_t>(4 * 148) * R * R * sizeof(double), 256));
       cur[i] = R;
       scratch = std::max(scratch, mode_gram_ws_bytes(make_dims(d, cur), i));
       cur[i] = ranks[i];
@@ -697,7 +700,18 @@ static int sthosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_
     ar.off = mark;
     // 3. B = G x_i Q^T: local; on the sharded mode the slab rows of Q, and the partial B is summed
     const float* Qrows = (dist && last) ? Qf + slab_begin * R : Qf;
-    KRP_TRY(ttm(G, cg, i, Qrows, R, 1, R, B, s, &ar));
+    // NEXT-3, the fused step: for the first mode (a mode-1 product on the tensor cores) the truncation's
+    // Gram B_(1) B_(1)^T is formed in the same pass, from the product's output tile in shared memory
+    const int64_t H0 = cg.N / cg.n[0];
+    const bool fused = i == 0 && ranks[i] < R && R <= 32 && ttm0_tc_ok(G, cg.n[0], H0, R) && ttm0_tc_grid(H0) <= 148;
+    if (fused) {
+      const int P = 4 * ttm0_tc_grid(H0);
+      double* gp = ar.take<double>(static_cast<size_t>(P) * R * R);
+      KRP_TRY(ttm0_tc(G, cg.n[0], H0, Qrows, R, 1, R, B, ar, s, 0, gp));
+      KRP_TRY(sum_partials_f64(gp, P, static_cast<int64_t>(R) * R, H, s));
+    } else {
+      KRP_TRY(ttm(G, cg, i, Qrows, R, 1, R, B, s, &ar));
+    }
     ar.off = mark;
     int64_t bd[kMaxD];
     for (int k = 0; k < d; ++k) bd[k] = cur[k];
@@ -708,7 +722,7 @@ static int sthosvd_impl(const float* X, const Dims& g, int64_t Id_global, int64_
     if (ranks[i] < R) {
       // 4. U = leading r_i left singular vectors of B_(i) (its Gram sums over the slabs for i < d-1);
       //    G <- B x_i U^T; Q_i = Q U
-      KRP_TRY(mode_gram(B, bg, i, H, ar, s));
+      if (!fused) KRP_TRY(mode_gram(B, bg, i, H, ar, s));
       ar.off = mark;
       if (dist && !last) KRP_TRY(allreduce_sum_f64(dc, H, static_cast<size_t>(R) * R, s));
       KRP_TRY(sym_eig_top(H, R, ranks[i], U, s));

@@ -49,10 +49,15 @@ int ttm(const float* X, const Dims& g, int n, const float* A, int J, int64_t sj,
 // I % 4 == 0, X 16-byte aligned; workspace: the B-operand image of A.  H1 > 0 (dividing H): the output is
 // written mode-permuted, Y[h1 + H1 (j + J h2)] for h = h1 + H1 h2, i.e. (I_2, J, I_3..) instead of
 // (J, I_2, I_3..), so the next contraction (over I_2) is again a mode-0 product.
+// gram_partials (J <= 32, unpermuted): also writes 4 per-CTA partials of the output's mode-1 Gram
+// Y_(1) Y_(1)ᵀ (fp64, J x J each, ttm0_tc_grid(H) * 4 of them) for a fixed-order sum.
 bool ttm0_tc_ok(const float* X, int64_t I, int64_t H, int J);
 size_t ttm0_tc_ws_bytes(int64_t I, int J);
+int ttm0_tc_grid(int64_t H);
 int ttm0_tc(const float* X, int64_t I, int64_t H, const float* A, int J, int64_t sj, int64_t si, float* Y, Arena& ar,
-            cudaStream_t s, int64_t H1 = 0);
+            cudaStream_t s, int64_t H1 = 0, double* gram_partials = nullptr);
+// out[idx] = sum_p partial[p * len + idx], fixed order (krp_linalg.cu)
+int sum_partials_f64(const double* partial, int P, int64_t len, double* out, cudaStream_t s);
 
 // H = T_(n) T_(n)^T (J x J, fp64) for T of dims g with J = g.n[n].
 size_t mode_gram_ws_bytes(const Dims& g, int n);

@@ -985,6 +985,12 @@ int cholqr(const float* Y, int64_t rows, int R, float* Qf, double* Qd, int* flag
   return KRP_OK;
 }
 
+int sum_partials_f64(const double* partial, int P, int64_t len, double* out, cudaStream_t s) {
+  sum_partials_f64_kernel<<<static_cast<unsigned>((len + 31) / 32), 1024, 0, s>>>(partial, P, len, out);
+  KRP_CHECK_LAUNCH();
+  return KRP_OK;
+}
+
 size_t ttm_ws_bytes(const Dims& g, int n, int J) {
   return (n == 0 && J >= 1 && J <= 64 && g.n[0] % 4 == 0) ? ttm0_tc_ws_bytes(g.n[0], J) : 0;
 }

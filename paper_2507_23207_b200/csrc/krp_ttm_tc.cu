@@ -65,6 +65,7 @@ struct Ttm0Params {
   const float* Bimg; // [nk][2 Np][32] swizzled: rows [0, Np) A_hi, [Np, 2Np) A_lo
   float* Y;
   int64_t H1;        // > 0: permuted output Y[h1 + H1 (j + J h2)] for h = h1 + H1 h2 (else Y[j + J h])
+  double* gram;      // non-null (J <= 32, H1 == 0): per-warp partial Grams of the output rows, [grid*4][J][J]
 };
 
 // round to the nearest tf32 (ties away from zero); the result has its 13 low mantissa bits clear
@@ -98,6 +99,14 @@ __global__ void ttm0_bimg_kernel(const float* __restrict__ A, int J, int I, int6
   }
 }
 
+// D (8x8, fp64) += A (8x4, row) B (4x8, col): the fp64 tensor-core MMA (one double of A and of B and two
+// of D per lane: A(t/4, t%4), B(t%4, t/4), D(t/4, 2(t%4) + {0, 1}))
+__device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
 __device__ __forceinline__ void t0_sts(uint32_t saddr, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(saddr), "f"(v) : "memory");
 }
@@ -112,7 +121,8 @@ __device__ __forceinline__ float t0_lds(uint32_t saddr) {
 #define KRP_T0_DBG 0  // development probes (results garbage): 1 epilogue skips TMEM, 2 split skips smem/ALU, 4 no MMAs
 #endif
 
-__global__ void __launch_bounds__(kT0Threads, 1)
+template <bool kGram>
+__global__ void __maxnreg__(168)  // 10 warps on 4 SM sub-partitions (3 + 3 + 2 + 2 x 32 x 168 <= 16384 each)
     ttm0_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Ttm0Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -279,6 +289,14 @@ __global__ void __launch_bounds__(kT0Threads, 1)
     const uint32_t wsa = smem_u32(stg + q * 32 * kT0MaxJ);  // this warp's 32 rows: the contiguous run Y[J h0, ...)
     int as = 0;
     uint32_t aph = 0;
+    // fused mode-1 Gram of the output (STHOSVD: the truncation needs B_(1) B_(1)ᵀ of B = X x_1 Qᵀ): the
+    // warp's 32 staged rows are 32 fibers; H += Σ_f b_f b_fᵀ by fp64 tensor-core MMAs (m8n8k4, K = 4
+    // fibers per step) on the 10 upper 8x8 blocks of the (J <= 32) x (J <= 32) Gram, accumulated in
+    // registers over all of the CTA's tiles in a fixed order
+    constexpr bool do_gram = kGram;
+    double g0[kGram ? 10 : 1], g1[kGram ? 10 : 1];
+#pragma unroll
+    for (int b = 0; b < (kGram ? 10 : 1); ++b) g0[b] = g1[b] = 0.0;
     for (int64_t t = t0; t < t1; ++t) {
       float acc[kT0MaxJ];
 #pragma unroll
@@ -331,6 +349,24 @@ __global__ void __launch_bounds__(kT0Threads, 1)
         for (int j = 0; j < kT0MaxJ; ++j)
           if (j < J) t0_sts(wrow + 4u * j, acc[j]);
         __syncwarp();
+        if constexpr (do_gram) {
+          // fragment of block row bi, fibers 4s..4s+3: element (8 bi + lane/4, fiber 4s + lane%4)
+          const int fr = static_cast<int>(lane) >> 2, fk = static_cast<int>(lane) & 3;
+#pragma unroll
+          for (int st4 = 0; st4 < 8; ++st4) {
+            double f[4];
+#pragma unroll
+            for (int bi = 0; bi < 4; ++bi) {
+              const int a = 8 * bi + fr;
+              f[bi] = a < J ? static_cast<double>(t0_lds(wsa + 4u * static_cast<uint32_t>((4 * st4 + fk) * J + a))) : 0.0;
+            }
+            int b = 0;
+#pragma unroll
+            for (int bi = 0; bi < 4; ++bi)
+#pragma unroll
+              for (int bj = bi; bj < 4; ++bj, ++b) dmma_884(g0[b], g1[b], f[bi], f[bj]);
+          }
+        }
         const int64_t nr = min(static_cast<int64_t>(32), p.H - h0);
         if (nr > 0) {
           float* out = p.Y + static_cast<int64_t>(J) * h0;
@@ -338,6 +374,26 @@ __global__ void __launch_bounds__(kT0Threads, 1)
           for (int e = static_cast<int>(lane); e < n; e += 32) out[e] = t0_lds(wsa + 4u * e);
         }
       }
+    }
+    if constexpr (do_gram) {
+      double* out = p.gram + (static_cast<int64_t>(blockIdx.x) * 4 + q) * J * J;
+      const int cr = static_cast<int>(lane) >> 2, cc = 2 * (static_cast<int>(lane) & 3);
+      int b = 0;
+#pragma unroll
+      for (int bi = 0; bi < 4; ++bi)
+#pragma unroll
+        for (int bj = bi; bj < 4; ++bj, ++b) {
+          const int r0 = 8 * bi + cr;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int c0 = 8 * bj + cc + e;
+            const double v = e ? g1[b] : g0[b];
+            if (r0 < J && c0 < J) {
+              out[r0 * J + c0] = v;
+              out[c0 * J + r0] = v;
+            }
+          }
+        }
     }
   }
   __syncthreads();
@@ -351,6 +407,8 @@ int round16i(int v) { return (v + 15) / 16 * 16; }
 
 }  // namespace
 
+int ttm0_tc_grid(int64_t H) { return static_cast<int>(std::min<int64_t>((H + kT0Rows - 1) / kT0Rows, device_sms())); }
+
 bool ttm0_tc_ok(const float* X, int64_t I, int64_t H, int J) {
   return tc_device_ok() && J >= 1 && J <= kT0MaxJ && I >= 1 && I % 4 == 0 && I < (int64_t(1) << 31) && H >= 1 &&
          H < (int64_t(1) << 31) && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
@@ -362,7 +420,7 @@ size_t ttm0_tc_ws_bytes(int64_t I, int J) {
 }
 
 int ttm0_tc(const float* X, int64_t I, int64_t H, const float* A, int J, int64_t sj, int64_t si, float* Y, Arena& ar,
-            cudaStream_t s, int64_t H1) {
+            cudaStream_t s, int64_t H1, double* gram_partials) {
   if (!ttm0_tc_ok(X, I, H, J)) {
     set_error("ttm0_tc: unsupported shape or device (I=%lld H=%lld J=%d)", static_cast<long long>(I),
               static_cast<long long>(H), J);
@@ -386,6 +444,11 @@ int ttm0_tc(const float* X, int64_t I, int64_t H, const float* A, int J, int64_t
   p.Bimg = img;
   p.Y = Y;
   p.H1 = (H1 > 0 && H % H1 == 0) ? H1 : 0;
+  p.gram = (gram_partials && J <= 32 && p.H1 == 0) ? gram_partials : nullptr;
+  if (gram_partials && !p.gram) {
+    set_error("ttm0_tc: the fused Gram needs J <= 32 and the unpermuted output");
+    return KRP_EINVAL;
+  }
   // shared memory: stages of (X box 16 KB + B image), the epilogue staging, barriers; ~200 KB
   const uint32_t stage = kT0Rows * 128 + p.b_bytes;
   const uint32_t stg_bytes = 4 * 32 * kT0MaxJ * 4;
@@ -420,10 +483,10 @@ int ttm0_tc(const float* X, int64_t I, int64_t H, const float* A, int J, int64_t
     ttm0_bimg_kernel<<<nb, 256, 0, s>>>(A, J, p.I, sj, si, p.Np, p.nk, img);
     KRP_CHECK_LAUNCH();
   }
-  KRP_CHECK_CUDA(cudaFuncSetAttribute(ttm0_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem_bytes)));
+  auto kern = p.gram ? ttm0_tc_kernel<true> : ttm0_tc_kernel<false>;
+  KRP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_bytes)));
   const int grid = static_cast<int>(std::min<int64_t>(p.T, device_sms()));
-  ttm0_tc_kernel<<<grid, kT0Threads, smem_bytes, s>>>(tmap, p);
+  kern<<<grid, kT0Threads, smem_bytes, s>>>(tmap, p);
   KRP_CHECK_LAUNCH();
   ar.off = mark;
   return KRP_OK;
