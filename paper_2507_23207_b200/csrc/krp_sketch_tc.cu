@@ -47,7 +47,19 @@ constexpr int kNumEpiWarps = 8;
 constexpr int kTmaWarp = 16;       // WG4: TMA producer, MMA issuer (owns the TMEM allocation), 2 idle warps
 constexpr int kMmaWarp = 17;
 constexpr int kThreads = 20 * 32;
-constexpr int kRegsSplit = 96, kRegsEpi = 128, kRegsProd = 32;  // the epilogue gains exactly what the producer group releases: 256*(128-96) = 128*(96-32)
+#ifndef KRP_REGS_PROD
+#define KRP_REGS_PROD 32
+#endif
+#ifndef KRP_REGS_EPI
+#define KRP_REGS_EPI 128
+#endif
+constexpr int kRegsSplit = 96, kRegsEpi = KRP_REGS_EPI, kRegsProd = KRP_REGS_PROD;
+// With the A1/A2 accumulators in TMEM or few of them in registers (RA <= 32) the epilogue fits in 112
+// registers and the TMA / MMA warps get 48 (at 32 the MMA issue loop spills: 65 local loads / stores in
+// <16, 0>, the c5 plan); wider register accumulators keep 128 / 32.  Budget: 256 x (epi - 96) <=
+// 128 x (96 - prod).
+constexpr int regs_prod(int ra) { return ra <= 32 ? 48 : kRegsProd; }
+constexpr int regs_epi(int ra) { return ra <= 32 ? 112 : kRegsEpi; }  // the epilogue gains exactly what the producer group releases: 256*(128-96) = 128*(96-32)
 constexpr int kTile = 128;
 constexpr int kStageFloats = 4 * 128 * 32;  // one 128x128 fp32 tile = 4 TMA boxes of {32, 128}
 constexpr int kMaxTcR = 64;
@@ -345,7 +357,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp >= kTmaWarp) {
   // producer warpgroup: one setmaxnreg for the whole group, then TMA / MMA / idle warps
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsProd));
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(regs_prod(RA)));
   if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer
     if (elect_one()) {
@@ -584,7 +596,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // warps 8-11: P side (z1 -> A1 += z1·Ω_S), warps 12-15: Q side (z2 -> A2 += z2·Ω_S); A1/A2 live
     // in TMEM (lane = ρ resp. γ).  T(s,r) = Σ_ρ z1·W_L = Σ_γ z2·W_R: its 8-column rounds alternate
     // between the two sides.
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsEpi));  // both epilogue WGs
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(regs_epi(RA)));  // both epilogue WGs
     pdl_wait();  // B images and Ω_S rows come from the tables kernel launched just before
     if (threadIdx.x == kEpiWarp0 * 32) KRP_TRACE(13, 58);  // tables visible
     const uint32_t ew = warp - kEpiWarp0;  // 0..7
