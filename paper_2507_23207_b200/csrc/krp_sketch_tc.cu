@@ -60,6 +60,10 @@ constexpr int kRegsSplit = 96, kRegsEpi = KRP_REGS_EPI, kRegsProd = KRP_REGS_PRO
 // 128 x (96 - prod).
 constexpr int regs_prod(int ra) { return ra <= 32 ? 48 : kRegsProd; }
 constexpr int regs_epi(int ra) { return ra <= 32 ? 112 : kRegsEpi; }  // the epilogue gains exactly what the producer group releases: 256*(128-96) = 128*(96-32)
+// QH plans (Q's A_hi staged in TMEM, register accumulators up to R8 = 64): the split warps give up 32
+// registers too, so the epilogue holds A1 / A2 (64 floats) and the W rows: 256*(152-96) = 256*(96-64) +
+// 128*(96-48).
+constexpr int kRegsSplitQH = 64, kRegsProdQH = 48, kRegsEpiQH = 152;
 constexpr int kTile = 128;
 constexpr int kStageFloats = 4 * 128 * 32;  // one 128x128 fp32 tile = 4 TMA boxes of {32, 128}
 constexpr int kMaxTcR = 64;
@@ -303,10 +307,15 @@ __device__ __forceinline__ void epi_round8(int rnd, float (&acc)[8], uint32_t tD
 //   acc_full[a]     the tile's accumulators are complete              (1 MMA commit; epilogue waits)
 //   acc_empty[a]    the epilogue drained accumulator stage a          (8 epilogue arrivals; MMA waits)
 //   b_ready         the segment's B images are in shared memory      (1 epilogue arrival; MMA waits)
-template <int CH, int RA>
+//
+// QH (Q's A_hi in TMEM): the split warps also store the raw tile with lane = γ, so no MMA reads the tile
+// stage; it is released as soon as the split warps have read it (they run up to NC chunks ahead of the
+// MMA), and the next tile's TMA overlaps the MMAs of the current one even with a single stage (NS = 1).
+template <int CH, int RA, bool QH = false>
 __global__ void __launch_bounds__(kThreads, 1)
     krp_tc_sketch_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ TcParams p) {
-  constexpr bool kSplitRoles = KRP_SPLIT_ROLES < 0 ? (RA == 0) : (KRP_SPLIT_ROLES != 0);
+  constexpr bool kSplitRoles = QH || (KRP_SPLIT_ROLES < 0 ? (RA == 0) : (KRP_SPLIT_ROLES != 0));
+  constexpr int kSlot = (QH ? 4 : 3) * CH;  // TMEM columns of one chunk slot: [P hi | P lo | Q lo (| Q hi)]
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* xs = reinterpret_cast<float*>(smem + p.sm_x);
@@ -330,7 +339,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < p.NS; ++i) {
       mbar_init(&full_x[i], 1);
-      mbar_init(&empty_x[i], kNumSplitWarps + 1);  // all split warps + the MMA warp's commit
+      mbar_init(&empty_x[i], QH ? kNumSplitWarps : kNumSplitWarps + 1);  // split warps (+ the MMA warp's commit)
     }
     for (int i = 0; i < p.NC; ++i) {
       mbar_init(&chunk_full[i], kSplitRoles ? kNumSplitWarps : 4);  // split warps writing this slot
@@ -357,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp >= kTmaWarp) {
   // producer warpgroup: one setmaxnreg for the whole group, then TMA / MMA / idle warps
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(regs_prod(RA)));
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(QH ? kRegsProdQH : regs_prod(RA)));
   if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer
     if (elect_one()) {
@@ -437,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (KRP_MMA_SPIN) HOT_WAIT(&chunk_full[cst], cph, KRP_MMA_SLEEP_NS); else KWAIT(&chunk_full[cst], cph);
         if (leader) KRP_TRACE(10, (t - t0) * 8 + kc);
         tc_fence_after();
-        const uint32_t ach = tbase + p.tm_chunk + cst * 3 * CH;  // [P hi | P lo | Q lo]
+        const uint32_t ach = tbase + p.tm_chunk + cst * kSlot;  // [P hi | P lo | Q lo (| Q hi)]
         const int kk0 = kc * (CH / 8);
         const uint64_t boff = static_cast<uint64_t>(kk0 >> 2) * katom_d + (kk0 & 3) * 2;
         // Q's A_hi: the raw tile in stage xst, box kk0/4 (16 KB), K offset (kk0 & 3) * 32 B
@@ -451,8 +460,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               mma_tf32_ts(dP, ach + 8 * ks, bd, idesc2, acc0);              // P: hi x hi
               mma_tf32_ts(dP, ach + 8 * ks, bd + lo_d, idesc2, 1u);         //    hi x lo
               mma_tf32_ts(dP, ach + CH + 8 * ks, bd, idesc2, 1u);           //    lo x hi
-              mma_tf32_ss(dQ, aq + ks * 2, bdq, idesc2, acc0);              // Q: hi (SMEM) x hi
-              mma_tf32_ss(dQ, aq + ks * 2, bdq + lo_d, idesc2, 1u);         //    hi x lo
+              if constexpr (QH) {
+                mma_tf32_ts(dQ, ach + 3 * CH + 8 * ks, bdq, idesc2, acc0);  // Q: hi (TMEM) x hi
+                mma_tf32_ts(dQ, ach + 3 * CH + 8 * ks, bdq + lo_d, idesc2, 1u);  //  hi x lo
+              } else {
+                mma_tf32_ss(dQ, aq + ks * 2, bdq, idesc2, acc0);            // Q: hi (SMEM) x hi
+                mma_tf32_ss(dQ, aq + ks * 2, bdq + lo_d, idesc2, 1u);       //    hi x lo
+              }
               mma_tf32_ts(dQ, ach + 2 * CH + 8 * ks, bdq, idesc2, 1u);      //    lo x hi
             }
           } else {
@@ -478,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       if (leader) {
-        mma_commit(&empty_x[xst]);  // the raw tile (Q's A_hi) may be overwritten once these MMAs finish
+        if constexpr (!QH) mma_commit(&empty_x[xst]);  // the raw tile (Q's A_hi) may be overwritten once these MMAs finish
         mma_commit(&acc_full[ast]);
         KRP_TRACE(4, t - t0);
       }
@@ -496,6 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ split warps: tile -> TMEM hi / lo
     // P view (lane = ρ): shared-memory loads (the transpose), hi = raw value, lo = x - tf32(x).
     // Q view (lane = γ): 16-byte loads of the rows; only lo goes to TMEM (Q's hi is read from SMEM).
+    if constexpr (QH) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsSplitQH));
     const uint32_t sub = warp & 3;
     // kSplitRoles: the two warps of a lane quarter share every chunk, warp w < 4 writing P hi / P lo and
     // warp w >= 4 Q lo (halves the split latency of a chunk); else warp w takes the chunks kc % 2 == w / 4.
@@ -533,7 +548,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (KRP_SPLIT_SPIN) HOT_WAIT(&chunk_ready[cst], cph ^ 1, KRP_SPLIT_SLEEP_NS); else KWAIT(&chunk_ready[cst], cph ^ 1);
         if (sub == 0 && lane == 0) KRP_TRACE(8, (t - t0) * 8 + kc);
         tc_fence_after();
-        const uint32_t ch = tbase + lane_off + p.tm_chunk + cst * 3 * CH;
+        const uint32_t ch = tbase + lane_off + p.tm_chunk + cst * kSlot;
         // P view: CH scalar loads (lane = ρ), hi stored as loaded, lo formed in place and stored
         if (dop) {
           uint32_t px[CH];
@@ -564,6 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             qv[4 * qq] = __float_as_uint(a0), qv[4 * qq + 1] = __float_as_uint(a1);
             qv[4 * qq + 2] = __float_as_uint(a2), qv[4 * qq + 3] = __float_as_uint(a3);
           }
+          if constexpr (QH) tmem_st<CH>(ch + 3 * CH, qv);  // Q hi: the raw value
 #pragma unroll
           for (int j = 0; j < CH; j += 2) {
             const float2 x = make_float2(__uint_as_float(qv[j]), __uint_as_float(qv[j + 1]));
@@ -596,7 +612,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // warps 8-11: P side (z1 -> A1 += z1·Ω_S), warps 12-15: Q side (z2 -> A2 += z2·Ω_S); A1/A2 live
     // in TMEM (lane = ρ resp. γ).  T(s,r) = Σ_ρ z1·W_L = Σ_γ z2·W_R: its 8-column rounds alternate
     // between the two sides.
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(regs_epi(RA)));  // both epilogue WGs
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(QH ? kRegsEpiQH : regs_epi(RA)));  // both epilogue WGs
     pdl_wait();  // B images and Ω_S rows come from the tables kernel launched just before
     if (threadIdx.x == kEpiWarp0 * 32) KRP_TRACE(13, 58);  // tables visible
     const uint32_t ew = warp - kEpiWarp0;  // 0..7
@@ -1086,6 +1102,7 @@ struct TcPlan {
   int RB = 0, CB = 0;
   int64_t T = 0;
   int R = 0, NP = 0, N2 = 0, R8 = 0, RS = 0, NS = 0, NC = 0, NA = 0, CH = 16, triple = 0, DN = 0, RA = 0;
+  int qh = 0;  // Q's A_hi staged in TMEM (chunk slots of 4*CH columns)
   int do_p = 0, do_q = 0, do_t = 0;
   int grid = 0, maxseg = 0, nslot = 0;
   int tm_acc = 0, tm_chunk = 0, tm_a = 0;
@@ -1161,20 +1178,26 @@ bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, bool allow
   // they do not live in registers.  The [hi|lo] concat form is 2 MMAs per K-step (DN = round16(R8 + R)),
   // the triple form 3 MMAs of N = N2 (DN = N2).  Large chunks amortise the split -> MMA handshake.
   {
+    // qh: Q's A_hi in TMEM too (register accumulators of R8 in (48, 64] only: the QH instantiations).  At
+    // R8 = 64 this is 4 slots of 4*16 columns next to the double-buffered triple-form accumulators, where
+    // the TMEM-accumulator plan has 2 slots of 3*16 and holds the tile stage until the MMAs finish.
     struct Opt {
-      int triple, na, ch, ncmin, areg;
-    } opts[9] = {{0, 2, 32, 2, 1}, {1, 2, 32, 3, 1}, {0, 2, 16, 4, 1}, {1, 2, 32, 2, 1}, {0, 2, 32, 2, 0},
-                 {0, 2, 16, 3, 0}, {1, 2, 32, 2, 0}, {1, 2, 16, 2, 0}, {1, 1, 16, 2, 0}};
+      int triple, na, ch, ncmin, areg, qh;
+    } opts[10] = {{0, 2, 32, 2, 1, 0}, {1, 2, 32, 3, 1, 0}, {0, 2, 16, 4, 1, 0}, {1, 2, 32, 2, 1, 0},
+                  {1, 2, 16, 4, 1, 1}, {0, 2, 32, 2, 0, 0}, {0, 2, 16, 3, 0, 0}, {1, 2, 32, 2, 0, 0},
+                  {1, 2, 16, 2, 0, 0}, {1, 1, 16, 2, 0, 0}};
     pl.NC = 0;
     const char* force = getenv("KRP_TC_OPT");  // development: force one option (if it fits)
     const int fo = force ? atoi(force) : -1;
-    for (int oi = 0; oi < 9; ++oi) {
+    for (int oi = 0; oi < 10; ++oi) {
       const Opt& o = opts[oi];
       if (fo >= 0 && oi != fo) continue;
-      if (o.areg && pl.R8 > 48) continue;  // register accumulators up to R = 48
+      if (o.areg && !o.qh && pl.R8 > 48) continue;  // register accumulators up to R = 48 ...
+      if (o.qh && (pl.R8 <= 48 || pl.R8 > 64)) continue;  // ... and R8 = 56, 64 in the QH form
       const int dn = o.triple ? pl.N2 : round16(pl.R8 + R);
       const int acols = o.areg ? 0 : 2 * pl.R8;
-      const int nc = std::min(o.ch == 16 ? 6 : 4, (512 - o.na * 2 * dn - acols) / (3 * o.ch));
+      const int slot = (o.qh ? 4 : 3) * o.ch;
+      const int nc = std::min(o.ch == 16 ? 6 : 4, (512 - o.na * 2 * dn - acols) / slot);
       if (nc >= o.ncmin) {
         pl.triple = o.triple;
         pl.DN = dn;
@@ -1182,6 +1205,7 @@ bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, bool allow
         pl.CH = o.ch;
         pl.NC = nc;
         pl.RA = o.areg ? pl.R8 : 0;
+        pl.qh = o.qh;
         break;
       }
     }
@@ -1190,7 +1214,7 @@ bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, bool allow
   }
   pl.tm_acc = 0;
   pl.tm_chunk = pl.NA * 2 * pl.DN;
-  pl.tm_a = pl.tm_chunk + pl.NC * 3 * pl.CH;
+  pl.tm_a = pl.tm_chunk + pl.NC * (pl.qh ? 4 : 3) * pl.CH;
   // SMEM: X stages (64 KB each), B_P and B_Q (NP rows x 512 B each), reduction scratch, barriers
   const uint32_t bbytes = static_cast<uint32_t>(pl.NP) * 512u;
   const uint32_t misc = 2 * 4 * kMaxTcR * 4 + 256 + 2 * kMaxTcR * 4;
@@ -1496,7 +1520,9 @@ int tc_sketch_cols(const float* X, const Dims& g, const OmegaPtrs& om, int R, in
   using KernFn = void (*)(const CUtensorMap, const TcParams);
   // register-accumulator variants are sized to R8 exactly (register pressure), all with CH = 32
   KernFn kern = nullptr;
-  if (pl.RA == 0) {
+  if (pl.qh) {
+    kern = pl.RA == 56 ? krp_tc_sketch_kernel<16, 56, true> : krp_tc_sketch_kernel<16, 64, true>;
+  } else if (pl.RA == 0) {
     kern = pl.CH == 32 ? krp_tc_sketch_kernel<32, 0> : krp_tc_sketch_kernel<16, 0>;
   } else {
     const bool c32 = pl.CH == 32;

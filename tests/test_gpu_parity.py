@@ -62,9 +62,10 @@ def test_integer_worked_example_bit_exact(krp):
         assert torch.equal(Y[n].cpu(), torch.from_numpy(ref[n].astype(np.float32))), n
 
 
-# tcgen05-tiled shapes with ragged blocks: d = 3, 4, 5, and R > 64 (two column groups)
+# tcgen05-tiled shapes with ragged blocks: d = 3, 4, 5, and R > 64 (two column groups); R = 60 / 56 take the
+# QH plan (Q's A_hi in TMEM, register accumulators), the c5 plan
 INT_SHAPES = [((256, 200, 12), 24), ((96, 64, 40, 10), 16), ((16, 12, 10, 8, 6), 8), ((128, 96, 20), 100),
-              ((384, 130, 3), 40)]
+              ((384, 130, 3), 40), ((256, 192, 10), 60), ((200, 130, 6), 56), ((64, 40, 36, 5), 60)]
 
 
 @pytest.mark.parametrize("dims,R", INT_SHAPES)
@@ -94,6 +95,7 @@ SHAPES = [
     ((256, 129, 3), 16), ((128, 128, 40), 40), ((256, 256, 17), 40), ((384, 128, 9), 64),
     ((16, 16, 16, 16, 16), 20), ((64, 64, 8, 8), 20), ((6, 5, 4, 3, 2, 2), 6), ((1000, 3), 2),
     ((128, 256, 7), 128), ((512, 128, 5), 30), ((200, 150, 6), 256), ((96, 80, 11), 65),
+    ((384, 256, 9), 60), ((130, 260, 5), 52), ((300, 200, 4), 120),
     # every mode odd: no grouping has a 16-byte row pitch (the repack path)
     ((5, 7, 9), 4), ((33, 35, 37), 12),
     # degenerate cases: R = 1, unit modes (first, middle, last), a single-element tensor, d = 2
