@@ -46,6 +46,8 @@ constexpr int kEpiWarp0 = 8;       // WG2-3: (P | Q side) x TMEM lane quarter
 constexpr int kNumEpiWarps = 8;
 constexpr int kTmaWarp = 16;       // WG4: TMA producer, MMA issuer (owns the TMEM allocation), 2 idle warps
 constexpr int kMmaWarp = 17;
+constexpr int kOmsWarp = 18;       // forms each tile's slice Khatri-Rao row Ω_S(s, ·) into a shared-memory ring
+constexpr int kOmsSlots = 4;
 constexpr int kThreads = 20 * 32;
 #ifndef KRP_REGS_PROD
 #define KRP_REGS_PROD 32
@@ -75,7 +77,6 @@ struct TcParams {
   int R, NP, N2, R8;  // NP: B-image rows; R8 = round8(R): row of B_lo / column of the hi·lo accumulator
   int triple;         // 1: three N=N2 MMAs into one accumulator (hh + hl + lh); 0: [hi|lo] concat (N=NP) + lo·hi
   int DN;             // accumulator columns per side (NP for concat, N2 for triple)
-  int RS;             // row stride (floats) of the OmS table: round4(R), a row is a 16 B-multiple bulk copy
   int NS, NC, NA;
   int do_p, do_q, do_t;
   int maxseg;  // max number of CTAs contributing to one (rb, cb) pair: partial slot = pair*maxseg + k
@@ -85,9 +86,12 @@ struct TcParams {
   float* partA2;
   int* slot_pair;  // [nslot]
   float* Tpart;    // [RB*CB][S][R]
-  const float* BPimg;  // [CB][NP*128]: W_R rows of col block cb, already in the SMEM B-operand layout
-  const float* BQimg;  // [RB][NP*128]: W_L rows of row block rb
-  const float* OmS;    // [S][RS]: Khatri-Rao rows of the slice modes
+  // the Ω_k (inputs, I_k x ldo row-major; null: a mode whose Ω is not given, factor 1) and the mode
+  // geometry: mode k of a group has index (lin / gs[k]) % n[k].  The Khatri-Rao rows W_L, W_R, Ω_S are
+  // formed from these on chip; no table of them exists in global memory.
+  const float* om[kMaxD];
+  uint32_t gn[kMaxD], ggs[kMaxD];
+  int d, m, m2, ldo;
   long long* trace;    // development timeline (KRP_TC_TRACE): CTA 0 role timestamps, null in production
   uint32_t wait_ns;    // mbarrier try_wait suspend-time hint (ns); 0 = spin
   int mma_spin;        // 1: the MMA warp polls its barriers without a suspend hint
@@ -140,6 +144,10 @@ __host__ __device__ __forceinline__ int cta_of_tile(int64_t t, int64_t T, int gr
 #define KRP_DBG(bit) ((p.dbg & (bit)) != 0)
 #define KRP_MMA_SPIN (p.mma_spin != 0)
 #define KRP_SPLIT_SPIN (p.split_spin != 0)
+#elif defined(KRP_PROBE_BITS)  // development: compile-time probes in an otherwise production build
+#define KRP_DBG(bit) ((KRP_PROBE_BITS & (bit)) != 0)
+#define KRP_MMA_SPIN true
+#define KRP_SPLIT_SPIN true
 #else
 #define KRP_DBG(bit) false
 #define KRP_MMA_SPIN true
@@ -159,6 +167,15 @@ __host__ __device__ __forceinline__ int cta_of_tile(int64_t t, int64_t T, int gr
 #endif
 #ifndef KRP_MMA_SLEEP_NS
 #define KRP_MMA_SLEEP_NS (RA >= 32 ? 32 : 0)
+#endif
+#ifndef KRP_BUILD_BATCH
+#define KRP_BUILD_BATCH 8
+#endif
+#ifndef KRP_SKETCH_PDL
+#define KRP_SKETCH_PDL 0
+#endif
+#ifndef KRP_SPLIT_BATCH
+#define KRP_SPLIT_BATCH 1
 #endif
 #ifndef KRP_SPLIT_SLEEP_NS
 #define KRP_SPLIT_SLEEP_NS 0
@@ -204,16 +221,14 @@ __device__ __forceinline__ void epi_drain8(int rnd, float (&z)[8], uint32_t tD, 
     z[j + 1] = v.y;
   }
 }
-__device__ __forceinline__ void epi_math8(int rnd, const float (&z)[8], float (&acc)[8], const float* __restrict__ oms_g,
+__device__ __forceinline__ void epi_math8(int rnd, const float (&z)[8], float (&acc)[8], uint32_t oms_s,
                                           bool my_t, const float (&w)[8], uint32_t rbuf_s, int R8, uint32_t sub,
                                           uint32_t lane) {
   const int rr = 8 * rnd;
   float om[8], tv[8];
-  {  // Ω_S(s, rr..rr+8): a broadcast, L1-resident global row (R8 floats, zero padded)
-    const float4 u = __ldg(reinterpret_cast<const float4*>(oms_g + rr));
-    const float4 v = __ldg(reinterpret_cast<const float4*>(oms_g + rr + 4));
-    om[0] = u.x, om[1] = u.y, om[2] = u.z, om[3] = u.w, om[4] = v.x, om[5] = v.y, om[6] = v.z, om[7] = v.w;
-  }
+  // Ω_S(s, rr..rr+8): the tile's slice Khatri-Rao row, formed by the MMA warp in shared memory (zero padded)
+  lds_v4(oms_s + rr * 4, om[0], om[1], om[2], om[3]);
+  lds_v4(oms_s + rr * 4 + 16, om[4], om[5], om[6], om[7]);
 #pragma unroll
   for (int j = 0; j < 8; j += 2) {
     const float2 zz = make_float2(z[j], z[j + 1]);
@@ -246,17 +261,14 @@ __device__ __forceinline__ void epi_math8(int rnd, const float (&z)[8], float (&
 }
 
 __device__ __forceinline__ void epi_round8(int rnd, float (&acc)[8], uint32_t tD, int R, int R8, int triple,
-                                           const float* __restrict__ oms_g, bool my_t, const float (&w)[8], uint32_t rbuf_s,
+                                           uint32_t oms_s, bool my_t, const float (&w)[8], uint32_t rbuf_s,
                                            uint32_t sub, uint32_t lane) {
   const int rr = 8 * rnd;
   float a[8], b[8], om[8], tv[8];
   tmem_ld8(tD + rr, a);
   if (!triple) tmem_ld8(tD + R8 + rr, b);
-  {  // Ω_S(s, rr..rr+8): a broadcast, L1-resident global row (R8 floats, zero padded)
-    const float4 u = __ldg(reinterpret_cast<const float4*>(oms_g + rr));
-    const float4 v = __ldg(reinterpret_cast<const float4*>(oms_g + rr + 4));
-    om[0] = u.x, om[1] = u.y, om[2] = u.z, om[3] = u.w, om[4] = v.x, om[5] = v.y, om[6] = v.z, om[7] = v.w;
-  }
+  lds_v4(oms_s + rr * 4, om[0], om[1], om[2], om[3]);  // Ω_S(s, rr..rr+8) (shared memory, zero padded)
+  lds_v4(oms_s + rr * 4 + 16, om[4], om[5], om[6], om[7]);
   tmem_ld_wait();
   const bool full = rr + 8 <= R;
 #pragma unroll
@@ -305,6 +317,8 @@ __device__ __forceinline__ void epi_round8(int rnd, float (&acc)[8], uint32_t tD
 //   chunk_ready[c]  chunk slot c is free: its previous MMAs are done  (1 MMA commit; split waits)
 //   chunk_full[c]   split wrote P hi / P lo / Q lo of the chunk       (4 split arrivals; MMA waits)
 //   acc_full[a]     the tile's accumulators are complete              (1 MMA commit; epilogue waits)
+//   oms_full[o]     the tile's Ω_S row is in ring slot o              (32 Ω_S-warp lanes; epilogue waits)
+//   oms_empty[o]    the epilogue is done with ring slot o             (8 epilogue warps; Ω_S warp waits)
 //   acc_empty[a]    the epilogue drained accumulator stage a          (8 epilogue arrivals; MMA waits)
 //   b_ready         the segment's B images are in shared memory      (1 epilogue arrival; MMA waits)
 //
@@ -314,7 +328,7 @@ __device__ __forceinline__ void epi_round8(int rnd, float (&acc)[8], uint32_t tD
 template <int CH, int RA, bool QH = false>
 __global__ void __launch_bounds__(kThreads, 1)
     krp_tc_sketch_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ TcParams p) {
-  constexpr bool kSplitRoles = QH || (KRP_SPLIT_ROLES < 0 ? (RA == 0) : (KRP_SPLIT_ROLES != 0));
+  constexpr bool kSplitRoles = KRP_SPLIT_ROLES < 0 ? (RA == 0 || QH) : (KRP_SPLIT_ROLES != 0);
   constexpr int kSlot = (QH ? 4 : 3) * CH;  // TMEM columns of one chunk slot: [P hi | P lo | Q lo (| Q hi)]
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -330,7 +344,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* acc_full = chunk_ready + p.NC;
   uint64_t* acc_empty = acc_full + p.NA;
   uint64_t* b_ready = acc_empty + p.NA;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(b_ready + 1);
+  uint64_t* oms_full = b_ready + 1;
+  uint64_t* oms_empty = oms_full + kOmsSlots;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(oms_empty + kOmsSlots);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -350,6 +366,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&acc_empty[i], kNumEpiWarps);
     }
     mbar_init(b_ready, 1);
+    for (int i = 0; i < kOmsSlots; ++i) {
+      mbar_init(&oms_full[i], 32);
+      mbar_init(&oms_empty[i], kNumEpiWarps);
+    }
     fence_barrier_init();
   }
   tc_fence_before();
@@ -358,6 +378,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tbase = *tmem_slot;
   if (threadIdx.x == 0) KRP_TRACE(13, 57);  // prologue done
   pdl_launch_dependents();  // the assembly kernel may be scheduled now (it waits for this grid to finish)
+#if KRP_SKETCH_PDL
+  pdl_wait();  // launched as a programmatic dependent: X and the Ω_k are read only after the previous grid
+#endif
 
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * p.T / gridDim.x;
   const int64_t t1 = static_cast<int64_t>(blockIdx.x + 1) * p.T / gridDim.x;
@@ -504,6 +527,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (++s_cur == p.S) s_cur = 0;
     }
+  } else if (warp == kOmsWarp) {
+    // ------------------------------------------------------------ Ω_S warp (otherwise idle)
+    // Ω_S(s, r) = Π_{k>=m2} Ω_k(i_k(s), r), lane r and r + 32, for each tile in order into ring slot
+    // (t - t0) % kOmsSlots: runs up to kOmsSlots tiles ahead of the epilogue, so the Ω loads' latency is
+    // off every other role's path.  The row is formed from the Ω_k inputs (never tabulated in HBM).
+    float* ring = reinterpret_cast<float*>(smem + p.sm_ws);
+    int o = 0;
+    uint32_t oph = 0;
+    uint32_t sl = static_cast<uint32_t>(t0 % p.S);
+    for (int64_t t = t0; t < t1 && !KRP_DBG(512); ++t) {
+      KWAIT(&oms_empty[o], oph ^ 1);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = static_cast<int>(lane) + 32 * h;
+        float w = r < p.R ? 1.f : 0.f;
+        if (r < p.R)
+          for (int k = p.m2; k < p.d; ++k)
+            if (p.om[k]) w *= __ldg(p.om[k] + static_cast<size_t>((sl / p.ggs[k]) % p.gn[k]) * p.ldo + r);
+        ring[o * kMaxTcR + r] = w;
+      }
+      mbar_arrive(&oms_full[o]);  // release: this lane's row entries
+      if (++o == kOmsSlots) {
+        o = 0;
+        oph ^= 1;
+      }
+      if (++sl == static_cast<uint32_t>(p.S)) sl = 0;
+    }
   }
   } else if (warp < kNumSplitWarps) {
     // (two split warps per lane quarter: warp w processes the chunks of slot w / 4, i.e. kc % 2 == w / 4)
@@ -539,18 +589,36 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     if (!kSplitRoles && par) advance();
     constexpr int kcStep = kSplitRoles ? 1 : 2;
+    // kBatch chunks per wait::st / fence / arrive round (roles mode): amortises the per-chunk handshake
+    constexpr int kBatch = kSplitRoles ? KRP_SPLIT_BATCH : 1;
     for (int64_t t = t0; t < t1; ++t) {
       KWAIT(&full_x[xst], xph);
       if (sub == 0 && lane == 0) KRP_TRACE(1, t - t0);
       const uint32_t stage_off = static_cast<uint32_t>(xst) * (kStageFloats * 4u);
-      for (int kc = kSplitRoles ? 0 : par; kc < nkc; kc += kcStep) {
-        if (sub == 0 && lane == 0) KRP_TRACE(13, (t - t0) * 8 + kc);
-        if (KRP_SPLIT_SPIN) HOT_WAIT(&chunk_ready[cst], cph ^ 1, KRP_SPLIT_SLEEP_NS); else KWAIT(&chunk_ready[cst], cph ^ 1);
-        if (sub == 0 && lane == 0) KRP_TRACE(8, (t - t0) * 8 + kc);
+      for (int kc0 = kSplitRoles ? 0 : par; kc0 < nkc; kc0 += kcStep * kBatch) {
+        if (sub == 0 && lane == 0) KRP_TRACE(13, (t - t0) * 8 + kc0);
+        int bst[kBatch];
+        {
+          int c = cst;
+          uint32_t ph = cph;
+#pragma unroll
+          for (int b = 0; b < kBatch; ++b) {
+            bst[b] = c;
+            if (KRP_SPLIT_SPIN) HOT_WAIT(&chunk_ready[c], ph ^ 1, KRP_SPLIT_SLEEP_NS); else KWAIT(&chunk_ready[c], ph ^ 1);
+            if (++c == p.NC) {
+              c = 0;
+              ph ^= 1;
+            }
+          }
+        }
+        if (sub == 0 && lane == 0) KRP_TRACE(8, (t - t0) * 8 + kc0);
         tc_fence_after();
-        const uint32_t ch = tbase + lane_off + p.tm_chunk + cst * kSlot;
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+        const int kc = kc0 + b;
+        const uint32_t ch = tbase + lane_off + p.tm_chunk + bst[b] * kSlot;
         // P view: CH scalar loads (lane = ρ), hi stored as loaded, lo formed in place and stored
-        if (dop) {
+        if (dop && !KRP_DBG(8) && !KRP_DBG(128)) {  // probe bits 8: no split work, 128: no P-view split
           uint32_t px[CH];
           const uint32_t goff = stage_off + static_cast<uint32_t>(kc * CH) * 128u;
 #pragma unroll
@@ -567,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st<CH>(ch + 1 * CH, px);
         }
         // Q view: lane = γ, columns ρ = kc*CH + j: CH consecutive ρ of row γ (16-byte chunks, swizzled)
-        if (doq) {
+        if (doq && !KRP_DBG(8)) {
           uint32_t qv[CH];
           const int rho0 = kc * CH;
           const uint32_t rowa = qrow + stage_off + static_cast<uint32_t>(rho0 >> 5) * 16384u;
@@ -589,15 +657,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           tmem_st<CH>(ch + 2 * CH, qv);  // Q lo
         }
-        if (sub == 0 && lane == 0) KRP_TRACE(15, (t - t0) * 8 + kc);
+        }  // batch
+        if (sub == 0 && lane == 0) KRP_TRACE(15, (t - t0) * 8 + kc0);
         tmem_st_wait();
-        if (sub == 0 && lane == 0) KRP_TRACE(9, (t - t0) * 8 + kc);
+        if (sub == 0 && lane == 0) KRP_TRACE(9, (t - t0) * 8 + kc0);
         tc_fence_before();
         __syncwarp();
-        if (sub == 0 && lane == 0) KRP_TRACE(12, (t - t0) * 8 + kc);
-        if (lane == 0) mbar_arrive(&chunk_full[cst]);
-        advance();
-        if (!kSplitRoles) advance();  // skip the other parity's chunk
+        if (sub == 0 && lane == 0) KRP_TRACE(12, (t - t0) * 8 + kc0);
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+          if (lane == 0) mbar_arrive(&chunk_full[cst]);
+          advance();
+          if (!kSplitRoles) advance();  // skip the other parity's chunk
+        }
       }
       __syncwarp();
       if (sub == 0 && lane == 0) KRP_TRACE(2, t - t0);
@@ -613,8 +685,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // in TMEM (lane = ρ resp. γ).  T(s,r) = Σ_ρ z1·W_L = Σ_γ z2·W_R: its 8-column rounds alternate
     // between the two sides.
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(QH ? kRegsEpiQH : regs_epi(RA)));  // both epilogue WGs
-    pdl_wait();  // B images and Ω_S rows come from the tables kernel launched just before
-    if (threadIdx.x == kEpiWarp0 * 32) KRP_TRACE(13, 58);  // tables visible
+
     const uint32_t ew = warp - kEpiWarp0;  // 0..7
     const uint32_t sub = warp & 3;         // TMEM lane quarter
     const bool pside = ew < 4;
@@ -626,12 +697,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int R = p.R, R8 = p.R8;
     const int nr = (R + 7) / 8;
     // my side's W (B_Q = W_L rows for the P side, B_P = W_R rows for the Q side) for the T rounds
-    uint32_t wsw[8];
-    {
-      const uint32_t wb = smem_u32((pside ? bq : bp) + katom * (p.NP * 128));
-#pragma unroll
-      for (int j = 0; j < 8; ++j) wsw[j] = wb + ((c0 ^ static_cast<uint32_t>(j)) << 4) + e0;
-    }
+    // this thread's k-atom of the image: row n's element sits at wb + n*128 + ((c0 ^ (n & 7)) << 4) + e0
+    const uint32_t wb = smem_u32((pside ? bq : bp) + katom * (p.NP * 128));
     const uint32_t tA = tbase + lane_off + p.tm_a + (pside ? 0 : R8);  // A1 / A2 columns
     // this lane's W row for this side's T rounds (P side: even rounds, Q side: odd rounds)
     constexpr int kRounds = RA > 0 ? RA / 8 : kMaxTcR / 8;
@@ -647,6 +714,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t aph = 0;
     int64_t prev_pair = -1;
     int seg = -1;
+    int oslot = 0;  // Ω_S ring slot of the current tile and its phase
+    uint32_t ooph = 0;
     int parity = 0;
     int64_t pair = t0 / p.S, s = t0 % p.S;  // advanced incrementally (no 64-bit division per tile)
     for (int64_t t = t0; t < t1; ++t, (++s == p.S ? (s = 0, ++pair) : 0)) {
@@ -685,15 +754,59 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int rnd = 0; rnd < nr; ++rnd) tmem_st8(tA + 8 * rnd, zero8);
           tmem_st_wait();
         }
-        // B operands of this segment: copy the pre-swizzled images (P side -> B_Q, Q side -> B_P)
+        // B operands of this segment, formed on chip (P side -> B_Q = W_L rows of row block rb, Q side ->
+        // B_P = W_R rows of col block cb): this thread's row lin = 128*blk + l of the group is the product of
+        // its modes' Ω rows, accumulated in place in the image's hi rows, then split hi / lo (UMMA K-major
+        // SWIZZLE_128B layout [k-atom][NP rows][128 B]; rows [R, R8) and [R8 + R, NP) are zero)
         {
-          const float4* src = reinterpret_cast<const float4*>(pside ? p.BQimg + rb * (p.NP * 128)
-                                                                    : p.BPimg + cb * (p.NP * 128));
-          float4* dst = reinterpret_cast<float4*>(pside ? bq : bp);
-          const int n4 = p.NP * 128 / 4;
-          const int me = static_cast<int>(sub * 32 + lane);
-#pragma unroll 8
-          for (int i = me; i < n4; i += 128) dst[i] = __ldg(src + i);
+          const uint32_t lin = static_cast<uint32_t>((pside ? rb : cb) * kTile) + static_cast<uint32_t>(l);
+          const bool inside = lin < static_cast<uint32_t>(pside ? p.M : p.C);
+          const int k0 = pside ? 0 : p.m, k1 = pside ? p.m : p.m2;
+          // the group's first two given modes' rows (independent loads in flight), further modes through a
+          // generic loop; Ω_n of a single-mode sketch is not given (factor 1)
+          const float* rowa = nullptr;
+          const float* rowb = nullptr;
+          int kx = k1;
+          if (inside)
+            for (int k = k0; k < k1; ++k) {
+              if (!p.om[k]) continue;
+              const float* row = p.om[k] + static_cast<size_t>((lin / p.ggs[k]) % p.gn[k]) * p.ldo;
+              if (!rowa) {
+                rowa = row;
+              } else if (!rowb) {
+                rowb = row;
+              } else {
+                kx = k;
+                break;
+              }
+            }
+          const uint32_t lo_row = static_cast<uint32_t>(R8) * 128u;
+          for (int r0 = 0; r0 < R8; r0 += 8) {
+            float v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const bool ok = r0 + j < R;
+              const float a = ok && rowa ? __ldg(rowa + r0 + j) : 1.f;
+              const float b = ok && rowb ? __ldg(rowb + r0 + j) : 1.f;
+              v[j] = ok && inside ? a * b : 0.f;
+            }
+            for (int k = kx; k < k1; ++k) {
+              if (!p.om[k]) continue;
+              const float* row = p.om[k] + static_cast<size_t>((lin / p.ggs[k]) % p.gn[k]) * p.ldo;
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if (r0 + j < R) v[j] *= __ldg(row + r0 + j);
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {  // rows r0 + j: (r0 + j) & 7 == j
+              const uint32_t ad = wb + ((c0 ^ static_cast<uint32_t>(j)) << 4) + e0 + static_cast<uint32_t>(r0 + j) * 128u;
+              const float whi = __uint_as_float(tf32_hi_bits(v[j]));
+              sts_f32(ad, whi);  // rows [R, R8): zero
+              if (r0 + j < R) sts_f32(ad + lo_row, v[j] - whi);
+            }
+          }
+          for (int r = R8 + R; r < p.NP; ++r)
+            sts_f32(wb + ((c0 ^ static_cast<uint32_t>(r & 7)) << 4) + e0 + static_cast<uint32_t>(r) * 128u, 0.f);
         }
         fence_proxy_async_smem();
         named_bar_sync(1, kNumEpiWarps * 32);
@@ -706,17 +819,27 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int rr = 8 * (2 * tr + (pside ? 0 : 1));
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-              const uint32_t ad = wsw[j] + (rr + j) * 128;
+              const uint32_t ad = wb + ((c0 ^ static_cast<uint32_t>(j)) << 4) + e0 + (rr + j) * 128;
               wreg[8 * tr + j] = rr + j < R ? lds_f32(ad) + lds_f32(ad + lo_row) : 0.f;
             }
           }
         }
       }
       KWAIT(&acc_full[ast], aph);
+      if (!KRP_DBG(512)) KWAIT(&oms_full[oslot], ooph);
+      const uint32_t oms_s = smem_u32(smem + p.sm_ws) + static_cast<uint32_t>(oslot * kMaxTcR) * 4u;
+      auto release_oms = [&]() {  // (after __syncwarp: every lane's reads of the row are done)
+        if (lane == 0 && !KRP_DBG(512)) mbar_arrive(&oms_empty[oslot]);
+        if (++oslot == kOmsSlots) {
+          oslot = 0;
+          ooph ^= 1;
+        }
+      };
       if (KRP_DBG(4)) {  // probe: no epilogue math
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[ast]);
+        release_oms();
         if (++ast == p.NA) {
           ast = 0;
           aph ^= 1;
@@ -726,7 +849,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (ew == 0 && lane == 0) KRP_TRACE(5, t - t0);
       tc_fence_after();
       const uint32_t tD = tbase + lane_off + p.tm_acc + ast * 2 * p.DN + (pside ? 0 : p.DN);
-      const float* oms_g = p.OmS + s * p.RS;
       const uint32_t rbuf_s = smem_u32(red + parity * (4 * R8));
       float* rbuf = red + parity * (4 * R8);
       bool released = false;
@@ -742,7 +864,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 8; ++j) w8[j] = wreg[8 * (rnd >> 1) + j];
             if (!KRP_DBG(64))  // probe bit 64: drain only
-            epi_math8(rnd, z8, acc8, oms_g, p.do_t && !KRP_DBG(32) && ((rnd & 1) == (pside ? 0 : 1)), w8, rbuf_s,
+            epi_math8(rnd, z8, acc8, oms_s, p.do_t && !KRP_DBG(32) && ((rnd & 1) == (pside ? 0 : 1)), w8, rbuf_s,
                       R8, sub, lane);
 #pragma unroll
             for (int j = 0; j < 8; ++j) Areg[8 * rnd + j] = acc8[j];
@@ -756,7 +878,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               float w8[8];  // register copy (no pointer into wreg)
 #pragma unroll
               for (int j = 0; j < 8; ++j) w8[j] = wreg[8 * (rnd >> 1) + j];
-              epi_round8(rnd, acc, tD, R, R8, p.triple, oms_g, p.do_t && ((rnd & 1) == (pside ? 0 : 1)), w8,
+              epi_round8(rnd, acc, tD, R, R8, p.triple, oms_s, p.do_t && ((rnd & 1) == (pside ? 0 : 1)), w8,
                          rbuf_s, sub, lane);
               uint32_t accb[8];
 #pragma unroll
@@ -772,6 +894,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[ast]);
       }
+      release_oms();
       if (++ast == p.NA) {
         ast = 0;
         aph ^= 1;
@@ -823,80 +946,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) KRP_TRACE(13, 61);  // kernel end
 }
 
-// ------------------------------------------------------------------ Khatri-Rao tables
-struct TabParams {
-  int d, m, m2, R, RS, R8, NP, RB, CB, ldo;
-  int64_t M, C, S;
-  int64_t n[kMaxD];
-  int64_t gs[kMaxD];
-  const float* om[kMaxD];
-  float *BPimg, *BQimg, *OmS;
-  int64_t T;
-  int grid, npairs;
-  int* pnk;  // [npairs]: CTAs (partial slots) that touch each (row block, col block) pair
-};
-
-// B-operand images in the exact shared-memory layout the UMMA descriptors expect (K-major,
-// SWIZZLE_128B, [k-atom][NP rows][128 B]): row n < R holds hi(W(lane, n)), row R8 + n holds
-// lo = W - hi, other rows are zero.  W_L(ρ,r) = Π_{k<m} Ω_k(i_k(ρ),r) for the row blocks (BQimg),
-// W_R(γ,r) = Π_{m<=k<m2} Ω_k(i_k(γ),r) for the col blocks (BPimg).  OmS(s,r) = Π_{k>=m2} Ω_k(i_k(s),r).
-__global__ void tc_tables_kernel(const __grid_constant__ TabParams p) {
-  // 32-bit index math throughout: the plan guarantees every table and group size is below 2^31
-  uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t per_blk = static_cast<uint32_t>(p.NP) * kTile;
-  const uint32_t nq = static_cast<uint32_t>(p.RB) * per_blk, np_ = static_cast<uint32_t>(p.CB) * per_blk;
-  const uint32_t ns = static_cast<uint32_t>(p.S) * static_cast<uint32_t>(p.RS);
-  if (idx < nq + np_) {
-    const bool rows = idx < nq;
-    if (!rows) idx -= nq;
-    const uint32_t blk = idx / per_blk;
-    const uint32_t rem = idx - blk * per_blk;
-    // rem enumerates (n, l) with l fastest
-    const int n = static_cast<int>(rem / kTile), l = static_cast<int>(rem % kTile);
-    const uint32_t lin = blk * kTile + l;
-    float v = 0.f;
-    const int r = n < p.R ? n : (n >= p.R8 && n < p.R8 + p.R ? n - p.R8 : -1);
-    if (r >= 0 && lin < static_cast<uint32_t>(rows ? p.M : p.C)) {
-      float w = 1.f;
-      for (int k = rows ? 0 : p.m; k < (rows ? p.m : p.m2); ++k) {
-        if (!p.om[k]) continue;  // Ω_n of a single-mode sketch is not given: it never reaches Y_n
-        const uint32_t ik = (lin / static_cast<uint32_t>(p.gs[k])) % static_cast<uint32_t>(p.n[k]);
-        w *= __ldg(p.om[k] + static_cast<size_t>(ik) * p.ldo + r);
-      }
-      const float whi = __uint_as_float(tf32_hi_bits(w));
-      v = (n < p.R) ? whi : w - whi;
-    }
-    const uint32_t k32 = static_cast<uint32_t>(l) & 31u;
-    const size_t off = static_cast<size_t>(l >> 5) * (p.NP * 128) + static_cast<size_t>(n) * 128 +
-                       (((k32 >> 2) ^ (static_cast<uint32_t>(n) & 7u)) << 4) + (k32 & 3u) * 4u;
-    float* img = (rows ? p.BQimg : p.BPimg) + static_cast<size_t>(blk) * per_blk;
-    *reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(img) + off) = v;
-  } else if ((idx -= nq + np_) < ns) {
-    const uint32_t sl = idx / static_cast<uint32_t>(p.RS);
-    const int r = static_cast<int>(idx - sl * static_cast<uint32_t>(p.RS));
-    float w = 0.f;
-    if (r < p.R) {
-      w = 1.f;
-      for (int k = p.m2; k < p.d; ++k) {
-        if (!p.om[k]) continue;
-        const uint32_t ik = (sl / static_cast<uint32_t>(p.gs[k])) % static_cast<uint32_t>(p.n[k]);
-        w *= __ldg(p.om[k] + static_cast<size_t>(ik) * p.ldo + r);
-      }
-    }
-    p.OmS[idx] = w;
-  } else if ((idx -= ns) < static_cast<uint32_t>(p.npairs)) {
-    const int64_t pr = idx;
-    p.pnk[idx] = cta_of_tile((pr + 1) * p.S - 1, p.T, p.grid) - cta_of_tile(pr * p.S, p.T, p.grid) + 1;
-  }
-}
-
 // ------------------------------------------------------------------ reduction of partials + multi-TTVs
 struct RedParams {
   int64_t M, C, S, T;
   int RB, CB, R, grid, maxseg, ldy;
   int do_p, do_q, do_t;
   const float *partA1, *partA2, *Tpart;
-  const int* pnk;  // slots used per pair (slots k >= pnk[pair] are not read)
   float *Pm, *Qc, *Ts;
   float *outP, *outQ, *outT;  // non-null: the group is a single wanted mode, write its Y directly
 };
@@ -968,7 +1023,8 @@ __global__ void __launch_bounds__(256) tc_assemble_kernel(const __grid_constant_
           const uint32_t f32 = static_cast<uint32_t>(ff), o = f32 / static_cast<uint32_t>(p.maxseg);
           const uint32_t k = f32 - o * static_cast<uint32_t>(p.maxseg);
           const int64_t pair = rows ? (static_cast<int64_t>(blk) * p.CB + o) : (static_cast<int64_t>(o) * p.CB + blk);
-          const int nk = spnk ? s_pnk[o] : __ldg(p.pnk + pair);
+          const int nk = spnk ? s_pnk[o]
+                              : cta_of_tile((pair + 1) * p.S - 1, p.T, p.grid) - cta_of_tile(pair * p.S, p.T, p.grid) + 1;
           if (static_cast<int>(k) < nk) v[i] = __ldg(part + (pair * p.maxseg + k) * kstride);
         }
       }
@@ -1101,7 +1157,7 @@ struct TcPlan {
                                         // a base address that is not 16-byte aligned)
   int RB = 0, CB = 0;
   int64_t T = 0;
-  int R = 0, NP = 0, N2 = 0, R8 = 0, RS = 0, NS = 0, NC = 0, NA = 0, CH = 16, triple = 0, DN = 0, RA = 0;
+  int R = 0, NP = 0, N2 = 0, R8 = 0, NS = 0, NC = 0, NA = 0, CH = 16, triple = 0, DN = 0, RA = 0;
   int qh = 0;  // Q's A_hi staged in TMEM (chunk slots of 4*CH columns)
   int do_p = 0, do_q = 0, do_t = 0;
   int grid = 0, maxseg = 0, nslot = 0;
@@ -1172,7 +1228,6 @@ bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, bool allow
   pl.do_p = (wr || ws) ? 1 : 0;  // T rounds alternate between z1 (P side) and z2 (Q side)
   pl.do_q = (wc || ws) ? 1 : 0;
   pl.R8 = (R + 7) / 8 * 8;
-  pl.RS = (R + 7) / 8 * 8;  // Ω_S rows padded to R8 (zeros) so the epilogue reads them as 16-byte vectors
   pl.N2 = round16(R);
   // TMEM (512 columns): NA accumulator stages of 2*DN, NC A-chunk stages of 4*CH, and A1 + A2 (2*R8) when
   // they do not live in registers.  The [hi|lo] concat form is 2 MMAs per K-step (DN = round16(R8 + R)),
@@ -1183,17 +1238,18 @@ bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, bool allow
     // the TMEM-accumulator plan has 2 slots of 3*16 and holds the tile stage until the MMAs finish.
     struct Opt {
       int triple, na, ch, ncmin, areg, qh;
-    } opts[10] = {{0, 2, 32, 2, 1, 0}, {1, 2, 32, 3, 1, 0}, {0, 2, 16, 4, 1, 0}, {1, 2, 32, 2, 1, 0},
+    } opts[12] = {{0, 2, 32, 2, 1, 0}, {1, 2, 32, 3, 1, 0}, {0, 2, 16, 4, 1, 0}, {1, 2, 32, 2, 1, 0},
                   {1, 2, 16, 4, 1, 1}, {0, 2, 32, 2, 0, 0}, {0, 2, 16, 3, 0, 0}, {1, 2, 32, 2, 0, 0},
-                  {1, 2, 16, 2, 0, 0}, {1, 1, 16, 2, 0, 0}};
+                  {1, 2, 16, 2, 0, 0}, {1, 1, 16, 2, 0, 0}, {0, 2, 16, 3, 1, 1}, {1, 2, 16, 3, 1, 1}};
     pl.NC = 0;
     const char* force = getenv("KRP_TC_OPT");  // development: force one option (if it fits)
     const int fo = force ? atoi(force) : -1;
-    for (int oi = 0; oi < 10; ++oi) {
+    for (int oi = 0; oi < 12; ++oi) {
       const Opt& o = opts[oi];
       if (fo >= 0 && oi != fo) continue;
       if (o.areg && !o.qh && pl.R8 > 48) continue;  // register accumulators up to R = 48 ...
-      if (o.qh && (pl.R8 <= 48 || pl.R8 > 64)) continue;  // ... and R8 = 56, 64 in the QH form
+      if (o.qh && (pl.R8 > 64 || (pl.R8 <= 48 && oi != fo))) continue;  // ... and R8 = 56, 64 in the QH form
+                                                                          // (R8 <= 48: development A/B only)
       const int dn = o.triple ? pl.N2 : round16(pl.R8 + R);
       const int acols = o.areg ? 0 : 2 * pl.R8;
       const int slot = (o.qh ? 4 : 3) * o.ch;
@@ -1217,7 +1273,7 @@ bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, bool allow
   pl.tm_a = pl.tm_chunk + pl.NC * (pl.qh ? 4 : 3) * pl.CH;
   // SMEM: X stages (64 KB each), B_P and B_Q (NP rows x 512 B each), reduction scratch, barriers
   const uint32_t bbytes = static_cast<uint32_t>(pl.NP) * 512u;
-  const uint32_t misc = 2 * 4 * kMaxTcR * 4 + 256 + 2 * kMaxTcR * 4;
+  const uint32_t misc = 2 * 4 * kMaxTcR * 4 + 256 + kOmsSlots * kMaxTcR * 4;
   const uint32_t budget = 232448 - 1024;
   int ns = static_cast<int>((budget - 2 * bbytes - misc) / (kStageFloats * 4));
   if (ns < 1) return false;
@@ -1228,7 +1284,7 @@ bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, bool allow
   pl.sm_red = pl.sm_bq + bbytes;
   pl.sm_bar = pl.sm_red + 2 * 4 * kMaxTcR * 4;
   pl.sm_ws = pl.sm_bar + 256;
-  pl.smem_bytes = pl.sm_ws + 2 * kMaxTcR * 4 + 1024;
+  pl.smem_bytes = pl.sm_ws + kOmsSlots * kMaxTcR * 4 + 1024;
   pl.grid = static_cast<int>(std::min<int64_t>(num_sms(), pl.T));
   // CTAs per (rb, cb) pair: a pair's S consecutive tiles meet at most ceil(S / floor(T/grid)) + 1
   // consecutive CTAs of the static split (each CTA owns >= floor(T/grid) consecutive tiles)
@@ -1286,7 +1342,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 long long* g_trace_dev = nullptr;
 
 struct WsLayout {
-  size_t a1, a2, slots, pnk, tpart, pm, qc, ts, wl, wr, oms, xp, total;
+  size_t a1, a2, slots, tpart, pm, qc, ts, xp, total;
 };
 WsLayout ws_layout(const TcPlan& pl) {
   WsLayout w{};
@@ -1300,14 +1356,10 @@ WsLayout ws_layout(const TcPlan& pl) {
   w.a1 = take(pl.do_p ? slotf : 0);
   w.a2 = take(pl.do_q ? slotf : 0);
   w.slots = take(static_cast<size_t>(pl.nslot) * sizeof(int));
-  w.pnk = take(static_cast<size_t>(pl.RB) * pl.CB * sizeof(int));
   w.tpart = take(pl.do_t ? static_cast<size_t>(pl.RB) * pl.CB * pl.S * pl.R * sizeof(float) : 0);
   w.pm = take(static_cast<size_t>(pl.M) * pl.R * sizeof(float));
   w.qc = take(static_cast<size_t>(pl.C) * pl.R * sizeof(float));
   w.ts = take(static_cast<size_t>(pl.S) * pl.R * sizeof(float));
-  w.wl = take(static_cast<size_t>(pl.RB) * pl.NP * kTile * sizeof(float));  // B_Q images
-  w.wr = take(static_cast<size_t>(pl.CB) * pl.NP * kTile * sizeof(float));  // B_P images
-  w.oms = take(static_cast<size_t>(pl.S) * pl.RS * sizeof(float));
   w.xp = take(pl.repack ? static_cast<size_t>(pl.Mp) * pl.C * pl.S * sizeof(float) : 0);
   w.total = off;
   return w;
@@ -1410,7 +1462,6 @@ int tc_sketch_cols(const float* X, const Dims& g, const OmegaPtrs& om, int R, in
   p.NP = pl.NP;
   p.N2 = pl.N2;
   p.R8 = pl.R8;
-  p.RS = pl.RS;
   p.triple = pl.triple;
   p.DN = pl.DN;
   p.NS = pl.NS;
@@ -1445,12 +1496,15 @@ int tc_sketch_cols(const float* X, const Dims& g, const OmegaPtrs& om, int R, in
   float* Pm = reinterpret_cast<float*>(wsb + wl.pm);
   float* Qc = reinterpret_cast<float*>(wsb + wl.qc);
   float* Ts = reinterpret_cast<float*>(wsb + wl.ts);
-  float* BQimg = reinterpret_cast<float*>(wsb + wl.wl);
-  float* BPimg = reinterpret_cast<float*>(wsb + wl.wr);
-  float* OmS = reinterpret_cast<float*>(wsb + wl.oms);
-  p.BQimg = BQimg;
-  p.BPimg = BPimg;
-  p.OmS = OmS;
+  p.d = g.d;
+  p.m = pl.m;
+  p.m2 = pl.m2;
+  p.ldo = ldo;
+  for (int k = 0; k < kMaxD; ++k) {
+    p.om[k] = k < g.d ? om.p[k] : nullptr;
+    p.gn[k] = k < g.d ? static_cast<uint32_t>(g.n[k]) : 1u;
+    p.ggs[k] = k < g.d ? static_cast<uint32_t>(gs[k]) : 1u;
+  }
   {
     const char* e = getenv("KRP_TC_DEBUG");
     p.dbg = e ? atoi(e) : 0;
@@ -1484,44 +1538,19 @@ int tc_sketch_cols(const float* X, const Dims& g, const OmegaPtrs& om, int R, in
       return KRP_ECUDA;
     }
   }
-  // 1. Khatri-Rao tables: B-operand images of every row / col block, and the slice-mode rows
-  {
-    TabParams tp{};
-    tp.d = g.d;
-    tp.m = pl.m;
-    tp.m2 = pl.m2;
-    tp.R = R;
-    tp.RS = pl.RS;
-    tp.R8 = pl.R8;
-    tp.NP = pl.NP;
-    tp.RB = pl.RB;
-    tp.CB = pl.CB;
-    tp.ldo = ldo;
-    tp.M = pl.M;
-    tp.C = pl.C;
-    tp.S = pl.S;
-    for (int k = 0; k < g.d; ++k) {
-      tp.n[k] = g.n[k];
-      tp.gs[k] = gs[k];
-      tp.om[k] = om.p[k];
-    }
-    tp.BPimg = BPimg;
-    tp.BQimg = BQimg;
-    tp.OmS = OmS;
-    tp.T = pl.T;
-    tp.grid = pl.grid;
-    tp.npairs = pl.RB * pl.CB;
-    tp.pnk = reinterpret_cast<int*>(wsb + wl.pnk);
-    const int64_t nt = (static_cast<int64_t>(pl.RB) + pl.CB) * pl.NP * kTile + pl.S * pl.RS + tp.npairs;
-    tc_tables_kernel<<<static_cast<unsigned>((nt + 255) / 256), 256, 0, s>>>(tp);
-    KRP_CHECK_LAUNCH();
-  }
-  // 2. the fused tile kernel
+  // 1. the fused tile kernel (the Khatri-Rao rows are formed on chip)
   using KernFn = void (*)(const CUtensorMap, const TcParams);
   // register-accumulator variants are sized to R8 exactly (register pressure), all with CH = 32
   KernFn kern = nullptr;
   if (pl.qh) {
-    kern = pl.RA == 56 ? krp_tc_sketch_kernel<16, 56, true> : krp_tc_sketch_kernel<16, 64, true>;
+    switch (pl.RA) {
+      case 24: kern = krp_tc_sketch_kernel<16, 24, true>; break;
+      case 32: kern = krp_tc_sketch_kernel<16, 32, true>; break;
+      case 40: kern = krp_tc_sketch_kernel<16, 40, true>; break;
+      case 56: kern = krp_tc_sketch_kernel<16, 56, true>; break;
+      case 64: kern = krp_tc_sketch_kernel<16, 64, true>; break;
+      default: set_error("tcgen05 sketch: no QH instantiation for R8 = %d", pl.RA); return KRP_EUNSUPPORTED;
+    }
   } else if (pl.RA == 0) {
     kern = pl.CH == 32 ? krp_tc_sketch_kernel<32, 0> : krp_tc_sketch_kernel<16, 0>;
   } else {
@@ -1538,7 +1567,12 @@ int tc_sketch_cols(const float* X, const Dims& g, const OmegaPtrs& om, int R, in
   KRP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(pl.smem_bytes)));
   prof_begin(s);
+#if KRP_SKETCH_PDL
   KRP_CHECK_CUDA(launch_pdl(kern, dim3(pl.grid), dim3(kThreads), pl.smem_bytes, s, tmap, p));
+#else
+  // a plain launch: the kernel reads X and the Ω_k, which the work before it in the stream may write
+  kern<<<pl.grid, kThreads, pl.smem_bytes, s>>>(tmap, p);
+#endif
   KRP_CHECK_LAUNCH();
   prof_end(s, 4.0 * static_cast<double>(g.N), 2.0 * static_cast<double>(g.N) * R * (pl.do_p + pl.do_q));
   if (p.trace) {  // development: dump CTA 0's role timeline (KRP_TC_TRACE=<file>)
@@ -1550,7 +1584,7 @@ int tc_sketch_cols(const float* X, const Dims& g, const OmegaPtrs& om, int R, in
       fclose(f);
     }
   }
-  // 3. fixed-order sum of the per-CTA partials, then the multi-TTVs of the three groups
+  // 2. fixed-order sum of the per-CTA partials, then the multi-TTVs of the three groups
   {
     RedParams rp{};
     rp.M = pl.M;
@@ -1569,7 +1603,6 @@ int tc_sketch_cols(const float* X, const Dims& g, const OmegaPtrs& om, int R, in
     rp.partA1 = p.partA1;
     rp.partA2 = p.partA2;
     rp.Tpart = p.Tpart;
-    rp.pnk = reinterpret_cast<const int*>(wsb + wl.pnk);
     rp.Pm = Pm;
     rp.Qc = Qc;
     rp.Ts = Ts;
