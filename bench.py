@@ -305,15 +305,17 @@ def run_ours(args, cfg, rank, world, local_rank):
         barrier()
         return max_over_ranks(ms), clocks
 
-    def kernel_profile(fn, steps, flush_l2=False):
-        """The dominant kernel's own event time (library profiler, events on the launching stream)."""
+    def timed_profiled(fn, steps, sampler=None, flush_l2=False):
+        """timed() with the library profiler on: CUDA events on the launching stream around every launch of
+        the dominant kernel INSIDE the timed region (so the kernel time and the step time see the same clocks
+        and power state).  Returns (step ms, clocks, (kernel ms, launches, alg bytes, alg flops))."""
         krp.krp_profile_reset()
         krp.krp_profile_enable(True)
-        timed(fn, steps, flush_l2=flush_l2)
+        ms, clocks = timed(fn, steps, sampler, flush_l2=flush_l2)
         krp.krp_profile_enable(False)
         r = krp.krp_profile_read()
         krp.krp_profile_reset()
-        return r
+        return ms, clocks, r
 
     # ---- phase A: the headline all-mode sketch
     for _ in range(args.warmup):
@@ -322,11 +324,12 @@ def run_ours(args, cfg, rank, world, local_rank):
     krp.krp_reset_launch_count()
     gpu_index = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local_rank)).split(",")[0]) \
         if os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")[0].isdigit() else local_rank
-    t_ms, clocks = timed(sketch, args.steps, ClockSampler(gpu_index) if rank == 0 else None, flush_l2=flush)
+    # the dominant kernel's own duration: CUDA events around each of its launches on the launching stream,
+    # recorded inside the timed region (a separate pass ran later, hotter, and read the kernel longer than
+    # the step it belongs to: r02d/r02f kernel_share_of_step 1.07-1.08 at c5)
+    t_ms, clocks, (k_ms, k_n, k_bytes, k_flops) = timed_profiled(
+        sketch, args.steps, ClockSampler(gpu_index) if rank == 0 else None, flush_l2=flush)
     launches = krp.krp_launch_count()
-    # the dominant kernel's own duration: a second pass with CUDA events around each of its launches (on the
-    # launching stream); kept out of the headline loop so the events do not perturb it
-    k_ms, k_n, k_bytes, k_flops = kernel_profile(sketch, args.steps, flush_l2=flush)
     flops_step = 4.0 * cfg.N * cfg.R
     value = flops_step * args.steps / (t_ms / 1e3) / 1e12
     roof = _roofline(dims_local, cfg.R, k_ms, k_n, k_bytes, k_flops, args.steps)
@@ -411,8 +414,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             for _ in range(3):
                 sk()
             nst = 10
-            tms, _ = timed(sk, nst)
-            kr = kernel_profile(sk, nst)
+            tms, _, kr = timed_profiled(sk, nst)
             rf = _roofline(c.dims, c.R, *kr, nst)
             entry = {"dims": list(c.dims), "R": c.R, "step_ms": tms / nst, "tflops_step": 4.0 * c.N * c.R / (tms / nst / 1e3) / 1e12,
                      "bound": rf["bound"], "achieved": rf["achieved"], "unit": rf["unit"], "frac": rf["frac"],

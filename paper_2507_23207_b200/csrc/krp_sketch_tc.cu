@@ -1238,13 +1238,14 @@ bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, bool allow
     // the TMEM-accumulator plan has 2 slots of 3*16 and holds the tile stage until the MMAs finish.
     struct Opt {
       int triple, na, ch, ncmin, areg, qh;
-    } opts[12] = {{0, 2, 32, 2, 1, 0}, {1, 2, 32, 3, 1, 0}, {0, 2, 16, 4, 1, 0}, {1, 2, 32, 2, 1, 0},
+    } opts[13] = {{0, 2, 32, 2, 1, 0}, {1, 2, 32, 3, 1, 0}, {0, 2, 16, 4, 1, 0}, {1, 2, 32, 2, 1, 0},
                   {1, 2, 16, 4, 1, 1}, {0, 2, 32, 2, 0, 0}, {0, 2, 16, 3, 0, 0}, {1, 2, 32, 2, 0, 0},
-                  {1, 2, 16, 2, 0, 0}, {1, 1, 16, 2, 0, 0}, {0, 2, 16, 3, 1, 1}, {1, 2, 16, 3, 1, 1}};
+                  {1, 2, 16, 2, 0, 0}, {1, 1, 16, 2, 0, 0}, {0, 2, 16, 3, 1, 1}, {1, 2, 16, 3, 1, 1},
+                  {1, 2, 32, 2, 1, 1}};
     pl.NC = 0;
     const char* force = getenv("KRP_TC_OPT");  // development: force one option (if it fits)
     const int fo = force ? atoi(force) : -1;
-    for (int oi = 0; oi < 12; ++oi) {
+    for (int oi = 0; oi < 13; ++oi) {
       const Opt& o = opts[oi];
       if (fo >= 0 && oi != fo) continue;
       if (o.areg && !o.qh && pl.R8 > 48) continue;  // register accumulators up to R = 48 ...
@@ -1542,7 +1543,13 @@ int tc_sketch_cols(const float* X, const Dims& g, const OmegaPtrs& om, int R, in
   using KernFn = void (*)(const CUtensorMap, const TcParams);
   // register-accumulator variants are sized to R8 exactly (register pressure), all with CH = 32
   KernFn kern = nullptr;
-  if (pl.qh) {
+  if (pl.qh && pl.CH == 32) {
+    switch (pl.RA) {
+      case 32: kern = krp_tc_sketch_kernel<32, 32, true>; break;
+      case 40: kern = krp_tc_sketch_kernel<32, 40, true>; break;
+      default: set_error("tcgen05 sketch: no QH instantiation for CH = 32, R8 = %d", pl.RA); return KRP_EUNSUPPORTED;
+    }
+  } else if (pl.qh) {
     switch (pl.RA) {
       case 24: kern = krp_tc_sketch_kernel<16, 24, true>; break;
       case 32: kern = krp_tc_sketch_kernel<16, 32, true>; break;
