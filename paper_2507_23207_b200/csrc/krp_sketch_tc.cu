@@ -1042,12 +1042,12 @@ __global__ void __launch_bounds__(256) tc_assemble_kernel(const __grid_constant_
     const int64_t p0 = w * npairs / kRedWarps, p1 = (w + 1) * npairs / kRedWarps;
     const int64_t pstride = p.S * p.R;
     const float* src = p.Tpart + s * p.R + r;
-    for (int64_t q = p0; q < p1; q += 8) {
-      float v[8];
+    for (int64_t q = p0; q < p1; q += 32) {  // 32 loads in flight: a share can be hundreds of pairs long
+      float v[32];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = (q + i < p1) ? __ldg(src + (q + i) * pstride) : 0.f;
+      for (int i = 0; i < 32; ++i) v[i] = (q + i < p1) ? __ldg(src + (q + i) * pstride) : 0.f;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc += v[i];
+      for (int i = 0; i < 32; ++i) acc += v[i];
     }
   }
   red[w][lane] = acc;
@@ -1236,21 +1236,25 @@ bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, bool allow
     // qh: Q's A_hi in TMEM too (register accumulators of R8 in (48, 64] only: the QH instantiations).  At
     // R8 = 64 this is 4 slots of 4*16 columns next to the double-buffered triple-form accumulators, where
     // the TMEM-accumulator plan has 2 slots of 3*16 and holds the tile stage until the MMAs finish.
+    // [rlo, rhi]: the R8 range where an option is taken by default (measured: the QH forms win at R8 = 32-64,
+    // profiles/r02e_*; at R8 <= 24 the concat register plan); KRP_TC_OPT forces one (if it fits)
     struct Opt {
-      int triple, na, ch, ncmin, areg, qh;
-    } opts[13] = {{0, 2, 32, 2, 1, 0}, {1, 2, 32, 3, 1, 0}, {0, 2, 16, 4, 1, 0}, {1, 2, 32, 2, 1, 0},
-                  {1, 2, 16, 4, 1, 1}, {0, 2, 32, 2, 0, 0}, {0, 2, 16, 3, 0, 0}, {1, 2, 32, 2, 0, 0},
-                  {1, 2, 16, 2, 0, 0}, {1, 1, 16, 2, 0, 0}, {0, 2, 16, 3, 1, 1}, {1, 2, 16, 3, 1, 1},
-                  {1, 2, 32, 2, 1, 1}};
+      int triple, na, ch, ncmin, areg, qh, rlo, rhi;
+    } opts[13] = {{1, 2, 32, 2, 1, 1, 32, 48}, {1, 2, 16, 4, 1, 1, 56, 64}, {0, 2, 32, 2, 1, 0, 8, 48},
+                  {1, 2, 32, 3, 1, 0, 8, 48},  {0, 2, 16, 4, 1, 0, 8, 48},  {1, 2, 32, 2, 1, 0, 8, 48},
+                  {0, 2, 32, 2, 0, 0, 8, 64},  {0, 2, 16, 3, 0, 0, 8, 64},  {1, 2, 32, 2, 0, 0, 8, 64},
+                  {1, 2, 16, 2, 0, 0, 8, 64},  {1, 1, 16, 2, 0, 0, 8, 64},  {0, 2, 16, 3, 1, 1, 0, 0},
+                  {1, 2, 16, 3, 1, 1, 0, 0}};
     pl.NC = 0;
     const char* force = getenv("KRP_TC_OPT");  // development: force one option (if it fits)
     const int fo = force ? atoi(force) : -1;
     for (int oi = 0; oi < 13; ++oi) {
       const Opt& o = opts[oi];
       if (fo >= 0 && oi != fo) continue;
-      if (o.areg && !o.qh && pl.R8 > 48) continue;  // register accumulators up to R = 48 ...
-      if (o.qh && (pl.R8 > 64 || (pl.R8 <= 48 && oi != fo))) continue;  // ... and R8 = 56, 64 in the QH form
-                                                                          // (R8 <= 48: development A/B only)
+      if (fo < 0 && (pl.R8 < o.rlo || pl.R8 > o.rhi)) continue;
+      if (o.areg && ((!o.qh && pl.R8 > 48) || pl.R8 > 64)) continue;  // register accumulators: R8 <= 48 (<= 64 QH)
+      if (o.qh && o.ch == 32 && (pl.R8 < 24 || pl.R8 > 48)) continue;  // the QH instantiations
+      if (o.qh && o.ch == 16 && pl.R8 != 24 && pl.R8 != 32 && pl.R8 != 40 && pl.R8 != 56 && pl.R8 != 64) continue;
       const int dn = o.triple ? pl.N2 : round16(pl.R8 + R);
       const int acols = o.areg ? 0 : 2 * pl.R8;
       const int slot = (o.qh ? 4 : 3) * o.ch;
@@ -1545,8 +1549,10 @@ int tc_sketch_cols(const float* X, const Dims& g, const OmegaPtrs& om, int R, in
   KernFn kern = nullptr;
   if (pl.qh && pl.CH == 32) {
     switch (pl.RA) {
+      case 24: kern = krp_tc_sketch_kernel<32, 24, true>; break;
       case 32: kern = krp_tc_sketch_kernel<32, 32, true>; break;
       case 40: kern = krp_tc_sketch_kernel<32, 40, true>; break;
+      case 48: kern = krp_tc_sketch_kernel<32, 48, true>; break;
       default: set_error("tcgen05 sketch: no QH instantiation for CH = 32, R8 = %d", pl.RA); return KRP_EUNSUPPORTED;
     }
   } else if (pl.qh) {

@@ -9,5 +9,5 @@ for c in $CFGS; do
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $OUT/launches_$c.csv \
     python tools/tc_time.py $c 3 > $OUT/ncu_launch_$c.log 2>&1; echo "rc=$?" >> $OUT/ncu_launch_$c.log
 done
-cuobjdump -sass paper_2507_23207_b200/libkrp.so > $OUT/libkrp.sass 2>/dev/null
+python tools/sass_counts.py > $OUT/sass_counts.txt 2>&1
 echo done

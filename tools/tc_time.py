@@ -6,7 +6,12 @@ import paper_2507_23207_b200 as krp
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
 check = len(sys.argv) > 3
-cfg = synth.config(name)
+if name.startswith("dims:"):  # dims:64,64,64,64,8:20 -> a random tensor of that shape, R = 20
+    _, ds, rs = name.split(":")
+    class _C: pass
+    cfg = _C(); cfg.dims = tuple(int(v) for v in ds.split(",")); cfg.R = int(rs); cfg.N = int(np.prod(cfg.dims))
+else:
+    cfg = synth.config(name)
 dims = cfg.dims
 xn = synth.random_tensor(dims, 1)
 x = torch.from_numpy(xn).cuda()
