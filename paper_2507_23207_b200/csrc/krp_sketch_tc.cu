@@ -958,51 +958,45 @@ struct RedParams {
 
 // P(ρ,r) = Σ_{cb} Σ_{k < pnk[pair]} partA1[(rb*CB + cb)*maxseg + k][r][ρ%128]
 // Qc(γ,r) likewise over rb;  Ts(s,r) = Σ_{pairs} Tpart[pair][s][r].
-// One block = 32 outputs x 8 warps: for P / Qc the 32 lanes take 32 consecutive rows ρ of one column r
-// (coalesced partial reads), for Ts 32 consecutive (s, r).  The flattened term list is split into 8
-// contiguous shares, each summed in order with its loads issued 8 at a time, then warp 0 adds the 8
-// shares in order: a fixed reduction tree (deterministic).  A block never straddles a 128-row block
-// (32 | 128) nor a region.  A group with a single mode IS that mode's sketch, so its region is written
-// straight into Y (outP / outQ / outT non-null).
+// P / Qc: one block = 32 consecutive rows (lanes: coalesced 128-byte partial reads) x 8/nsplit columns; the
+// F = (other blocks) x maxseg terms of a column are split into nsplit contiguous shares (one warp each, 16
+// loads in flight, (o, k) advanced incrementally), and the shares are added in order: a fixed reduction
+// order (deterministic).  nsplit grows with F so short term lists do not pay a block per column.
+// Ts: one block = 32 consecutive (s, r), the pair list split over the 8 warps (16 loads in flight), added in
+// order.  32-bit index math throughout (the plan keeps every group and table below 2^31); the slot counts
+// pnk follow from the static tile split and are formed per block before the wait on the sketch kernel.
+// A block never straddles a 128-row block (32 | 128) nor a region; a group with a single mode IS that
+// mode's sketch, so its region is written straight into Y (outP / outQ / outT non-null).
 constexpr int kRedWarps = 8;
 constexpr int kAsmMaxOther = 1024;
-__global__ void __launch_bounds__(256) tc_assemble_kernel(const __grid_constant__ RedParams p) {
+__host__ __device__ __forceinline__ int asm_nsplit(int64_t F) {
+  return F <= 32 ? 1 : (F <= 64 ? 2 : (F <= 128 ? 4 : 8));
+}
+__host__ __device__ __forceinline__ int64_t asm_region_blocks(int64_t rows, int R, int64_t F) {
+  const int cpb = kRedWarps / asm_nsplit(F);
+  return (rows + 31) / 32 * ((R + cpb - 1) / cpb);
+}
+__global__ void __launch_bounds__(256, 4) tc_assemble_kernel(const __grid_constant__ RedParams p) {
   __shared__ float red[kRedWarps][32];
   __shared__ int s_pnk[kAsmMaxOther];  // slots used by each pair this block reads (computed, not loaded)
   const int w = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
-  const int64_t nP = p.do_p ? p.M * p.R : 0, nQ = p.do_q ? p.C * p.R : 0, nT = p.do_t ? p.S * p.R : 0;
-  const int64_t bP = p.do_p ? (p.M + 31) / 32 * p.R : 0, bQ = p.do_q ? (p.C + 31) / 32 * p.R : 0;
-  int64_t blk_id = blockIdx.x;
-  int region;
-  if (blk_id < bP) {
-    region = 0;
-  } else if ((blk_id -= bP) < bQ) {
-    region = 1;
-  } else {
-    blk_id -= bQ;
-    region = 2;
-  }
-  int64_t idx = blk_id * 32 + lane;  // Ts: linear (s, r); P / Qc: replaced by rho * R + r below
-  bool valid = true;
-  float acc = 0.f;
-  int64_t outi = 0;  // output row (ρ, γ or s) and column, for the strided direct write into Y
-  int outr = 0;
-  if (region < 2) {
-    const bool rows = region == 0;
-    const int64_t nrow = rows ? p.M : p.C;
-    const int r = static_cast<int>(blk_id % p.R);
-    const int64_t rho = (blk_id / p.R) * 32 + lane;
-    valid = rho < nrow;
-    const int64_t rc = valid ? rho : nrow - 1;
-    idx = rc * p.R + r;
-    outi = rc;
-    outr = r;
-    const int blk = static_cast<int>(rc / kTile), l = static_cast<int>(rc % kTile);
-    const float* part = (rows ? p.partA1 : p.partA2) + static_cast<int64_t>(r) * kTile + l;
-    const int64_t kstride = static_cast<int64_t>(kTile) * p.R;
+  const int64_t FP = static_cast<int64_t>(p.CB) * p.maxseg, FQ = static_cast<int64_t>(p.RB) * p.maxseg;
+  const int64_t bP = p.do_p ? asm_region_blocks(p.M, p.R, FP) : 0, bQ = p.do_q ? asm_region_blocks(p.C, p.R, FQ) : 0;
+  uint32_t blk_id = blockIdx.x;
+  if (blk_id < bP + bQ) {
+    const bool rows = blk_id < bP;
+    if (!rows) blk_id -= static_cast<uint32_t>(bP);
     const int nother = rows ? p.CB : p.RB;
-    // the slot counts of this block's pairs follow from the static tile split (pure arithmetic), so they
-    // are formed before the wait on the sketch kernel instead of being loaded after it
+    const uint32_t F = static_cast<uint32_t>(rows ? FP : FQ);
+    const int nsplit = asm_nsplit(F), cpb = kRedWarps / nsplit;
+    const uint32_t ncg = static_cast<uint32_t>((p.R + cpb - 1) / cpb);
+    const uint32_t rg = blk_id / ncg, cg = blk_id - rg * ncg;
+    const uint32_t nrow = static_cast<uint32_t>(rows ? p.M : p.C);
+    const uint32_t rho = rg * 32u + static_cast<uint32_t>(lane);
+    const bool valid = rho < nrow;
+    const uint32_t rc = valid ? rho : nrow - 1;
+    const uint32_t blk = rc / kTile, l = rc % kTile;
+    const int r = static_cast<int>(cg) * cpb + w / nsplit, share = w % nsplit;
     const bool spnk = nother <= kAsmMaxOther;
     if (spnk)
       for (int o = static_cast<int>(threadIdx.x); o < nother; o += blockDim.x) {
@@ -1011,44 +1005,64 @@ __global__ void __launch_bounds__(256) tc_assemble_kernel(const __grid_constant_
       }
     __syncthreads();
     pdl_wait();  // the partials are written by the sketch kernel
-    const int64_t F = static_cast<int64_t>(nother) * p.maxseg;  // flattened (other block, slot) terms
-    const int64_t f0 = w * F / kRedWarps, f1 = (w + 1) * F / kRedWarps;
-    for (int64_t f = f0; f < f1; f += 8) {
-      float v[8];
+    float acc = 0.f;
+    if (r < p.R) {
+      const float* part = (rows ? p.partA1 : p.partA2) + static_cast<int64_t>(r) * kTile + l;
+      const int64_t kstride = static_cast<int64_t>(kTile) * p.R;
+      const uint32_t f0 = static_cast<uint32_t>(share) * F / static_cast<uint32_t>(nsplit);
+      const uint32_t f1 = static_cast<uint32_t>(share + 1) * F / static_cast<uint32_t>(nsplit);
+      uint32_t o = f0 / static_cast<uint32_t>(p.maxseg);
+      int k = static_cast<int>(f0 - o * static_cast<uint32_t>(p.maxseg));
+      for (uint32_t f = f0; f < f1; f += 16) {
+        float v[16];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        v[i] = 0.f;
-        const int64_t ff = f + i;
-        if (ff < f1) {
-          const uint32_t f32 = static_cast<uint32_t>(ff), o = f32 / static_cast<uint32_t>(p.maxseg);
-          const uint32_t k = f32 - o * static_cast<uint32_t>(p.maxseg);
-          const int64_t pair = rows ? (static_cast<int64_t>(blk) * p.CB + o) : (static_cast<int64_t>(o) * p.CB + blk);
-          const int nk = spnk ? s_pnk[o]
-                              : cta_of_tile((pair + 1) * p.S - 1, p.T, p.grid) - cta_of_tile(pair * p.S, p.T, p.grid) + 1;
-          if (static_cast<int>(k) < nk) v[i] = __ldg(part + (pair * p.maxseg + k) * kstride);
+        for (int i = 0; i < 16; ++i) {
+          v[i] = 0.f;
+          if (f + i < f1) {
+            const uint32_t pair = rows ? blk * static_cast<uint32_t>(p.CB) + o : o * static_cast<uint32_t>(p.CB) + blk;
+            const int nk = spnk ? s_pnk[o]
+                                : cta_of_tile((static_cast<int64_t>(pair) + 1) * p.S - 1, p.T, p.grid) -
+                                      cta_of_tile(static_cast<int64_t>(pair) * p.S, p.T, p.grid) + 1;
+            if (k < nk) v[i] = __ldg(part + (static_cast<int64_t>(pair) * p.maxseg + k) * kstride);
+            if (++k == p.maxseg) {
+              k = 0;
+              ++o;
+            }
+          }
         }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc += v[i];  // unused slots add an exact 0
       }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc += v[i];
     }
-  } else {
-    pdl_wait();  // Tpart is written by the sketch kernel
-    const uint32_t idc = static_cast<uint32_t>(idx < nT ? idx : nT - 1);
-    const uint32_t s = idc / static_cast<uint32_t>(p.R);
-    const int r = static_cast<int>(idc - s * static_cast<uint32_t>(p.R));
-    outi = s;
-    outr = r;
-    const int64_t npairs = static_cast<int64_t>(p.RB) * p.CB;
-    const int64_t p0 = w * npairs / kRedWarps, p1 = (w + 1) * npairs / kRedWarps;
-    const int64_t pstride = p.S * p.R;
-    const float* src = p.Tpart + s * p.R + r;
-    for (int64_t q = p0; q < p1; q += 32) {  // 32 loads in flight: a share can be hundreds of pairs long
-      float v[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = (q + i < p1) ? __ldg(src + (q + i) * pstride) : 0.f;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) acc += v[i];
+    red[w][lane] = acc;
+    __syncthreads();
+    if (share == 0 && r < p.R && valid) {
+      float tot = red[w][lane];
+      for (int i = 1; i < nsplit; ++i) tot += red[w + i][lane];
+      float* direct = rows ? p.outP : p.outQ;
+      if (direct) direct[static_cast<int64_t>(rc) * p.ldy + r] = tot;  // a single-mode group: its Y (stride ldy)
+      else (rows ? p.Pm : p.Qc)[static_cast<int64_t>(rc) * p.R + r] = tot;
     }
+    return;
+  }
+  blk_id -= static_cast<uint32_t>(bP + bQ);
+  const uint32_t nT = static_cast<uint32_t>(p.S) * static_cast<uint32_t>(p.R);
+  const uint32_t idx = blk_id * 32u + static_cast<uint32_t>(lane);
+  pdl_wait();  // Tpart is written by the sketch kernel
+  const uint32_t idc = idx < nT ? idx : nT - 1;
+  const uint32_t sl = idc / static_cast<uint32_t>(p.R);
+  const int r = static_cast<int>(idc - sl * static_cast<uint32_t>(p.R));
+  const int64_t npairs = static_cast<int64_t>(p.RB) * p.CB;
+  const int64_t p0 = w * npairs / kRedWarps, p1 = (w + 1) * npairs / kRedWarps;
+  const int64_t pstride = p.S * p.R;
+  const float* src = p.Tpart + static_cast<int64_t>(idc);
+  float acc = 0.f;
+  for (int64_t q = p0; q < p1; q += 16) {  // 16 loads in flight: a share can be hundreds of pairs long
+    float v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = (q + i < p1) ? __ldg(src + (q + i) * pstride) : 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc += v[i];
   }
   red[w][lane] = acc;
   __syncthreads();
@@ -1056,17 +1070,17 @@ __global__ void __launch_bounds__(256) tc_assemble_kernel(const __grid_constant_
     float tot = red[0][lane];
 #pragma unroll
     for (int i = 1; i < kRedWarps; ++i) tot += red[i][lane];
-    const int64_t n = region == 0 ? nP : (region == 1 ? nQ : nT);
-    float* direct = region == 0 ? p.outP : (region == 1 ? p.outQ : p.outT);
-    if (valid && idx < n) {
-      if (direct) direct[outi * p.ldy + outr] = tot;  // a single-mode group: its Y (row stride ldy)
-      else (region == 0 ? p.Pm : (region == 1 ? p.Qc : p.Ts))[idx] = tot;
+    if (idx < nT) {
+      if (p.outT) p.outT[static_cast<int64_t>(sl) * p.ldy + r] = tot;  // a single-mode group: its Y
+      else p.Ts[idx] = tot;
     }
   }
 }
 
-int64_t assemble_blocks(int64_t M, int64_t C, int64_t S, int R, int do_p, int do_q, int do_t) {
-  return (do_p ? (M + 31) / 32 * R : 0) + (do_q ? (C + 31) / 32 * R : 0) + (do_t ? (S * R + 31) / 32 : 0);
+int64_t assemble_blocks(int64_t M, int64_t C, int64_t S, int R, int do_p, int do_q, int do_t, int RB, int CB,
+                        int maxseg) {
+  return (do_p ? asm_region_blocks(M, R, static_cast<int64_t>(CB) * maxseg) : 0) +
+         (do_q ? asm_region_blocks(C, R, static_cast<int64_t>(RB) * maxseg) : 0) + (do_t ? (S * R + 31) / 32 : 0);
 }
 
 struct TtvParams {
@@ -1628,7 +1642,7 @@ int tc_sketch_cols(const float* X, const Dims& g, const OmegaPtrs& om, int R, in
       Ts = p.Tpart;
       rp.do_t = 0;
     }
-    const int64_t nblk = assemble_blocks(pl.M, pl.C, pl.S, R, rp.do_p, rp.do_q, rp.do_t);
+    const int64_t nblk = assemble_blocks(pl.M, pl.C, pl.S, R, rp.do_p, rp.do_q, rp.do_t, pl.RB, pl.CB, pl.maxseg);
     KRP_CHECK_CUDA(launch_pdl(tc_assemble_kernel, dim3(static_cast<unsigned>(nblk)), dim3(256), 0, s, rp));
     KRP_CHECK_LAUNCH();
   }
