@@ -1203,7 +1203,6 @@ const DevInfo& dev_info() {
 int num_sms() { return dev_info().sms; }
 bool device_is_sm100() { return dev_info().sm100; }
 
-int round16(int v) { return (v + 15) / 16 * 16; }
 
 // Fill geometry for a grouping (m, m2) and check the kernel's constraints.  Group sizes below 128 are
 // covered by TMA's out-of-bounds zero fill (partial row / column blocks); a row pitch that is not a multiple
@@ -1242,9 +1241,11 @@ bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, bool allow
   pl.do_p = (wr || ws) ? 1 : 0;  // T rounds alternate between z1 (P side) and z2 (Q side)
   pl.do_q = (wc || ws) ? 1 : 0;
   pl.R8 = (R + 7) / 8 * 8;
-  pl.N2 = round16(R);
+  // MMA N in steps of 8 (tcgen05, M = 128, cta_group::1: any multiple of 8 up to 256): N = R8, not round16(R)
+  // (c2's R = 40: 48 -> 40 columns, sketch kernel 145.8 -> 136.1 us)
+  pl.N2 = pl.R8;
   // TMEM (512 columns): NA accumulator stages of 2*DN, NC A-chunk stages of 4*CH, and A1 + A2 (2*R8) when
-  // they do not live in registers.  The [hi|lo] concat form is 2 MMAs per K-step (DN = round16(R8 + R)),
+  // they do not live in registers.  The [hi|lo] concat form is 2 MMAs per K-step (DN = round8(R8 + R)),
   // the triple form 3 MMAs of N = N2 (DN = N2).  Large chunks amortise the split -> MMA handshake.
   {
     // qh: Q's A_hi in TMEM too (register accumulators of R8 in (48, 64] only: the QH instantiations).  At
@@ -1269,7 +1270,7 @@ bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, bool allow
       if (o.areg && ((!o.qh && pl.R8 > 48) || pl.R8 > 64)) continue;  // register accumulators: R8 <= 48 (<= 64 QH)
       if (o.qh && o.ch == 32 && (pl.R8 < 24 || pl.R8 > 48)) continue;  // the QH instantiations
       if (o.qh && o.ch == 16 && pl.R8 != 24 && pl.R8 != 32 && pl.R8 != 40 && pl.R8 != 56 && pl.R8 != 64) continue;
-      const int dn = o.triple ? pl.N2 : round16(pl.R8 + R);
+      const int dn = o.triple ? pl.N2 : (pl.R8 + R + 7) / 8 * 8;
       const int acols = o.areg ? 0 : 2 * pl.R8;
       const int slot = (o.qh ? 4 : 3) * o.ch;
       const int nc = std::min(o.ch == 16 ? 6 : 4, (512 - o.na * 2 * dn - acols) / slot);
