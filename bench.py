@@ -221,7 +221,9 @@ def _traffic(name, world):
     if os.path.exists(tpath):
         with open(tpath) as f:
             tj = json.load(f)
-        ent = tj.get(f"{name}:{world}") or tj.get(name)
+        # a capture is per launch of one GPU's kernel: the whole-tensor entry holds for N = 1 only (a rank's
+        # slab launch moves 1/N of it); N > 1 needs its own "<cfg>:<N>" entry, else traffic is null
+        ent = tj.get(f"{name}:{world}") or (tj.get(name) if world == 1 else None)
         if ent:
             return ent.get("dram_bytes_per_launch")
     return None
