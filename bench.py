@@ -341,6 +341,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     # ---- phase B: full rHOSVD steps (sketch + QR + core + truncation) on the headline tensor
     rhosvd_s = None
     rel_err = None
+    rh_clocks = None
     if not args.no_rhosvd:
         if world > 1:
             wsr = torch.empty(krp.krp_workspace_bytes_dist(krp.OP_RHOSVD, dims_local, Id, cfg.R, cfg.ranks),
@@ -359,7 +360,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         for _ in range(min(args.warmup, 2)):
             rh()
         steps_b = max(1, min(args.steps, 10))
-        tb, _ = timed(rh, steps_b)
+        tb, rh_clocks = timed(rh, steps_b, ClockSampler(gpu_index) if rank == 0 else None)
         rhosvd_s = tb / 1e3 / steps_b
         del wsr
         rel_err = rh(with_error=True)[2]
@@ -457,7 +458,8 @@ def run_ours(args, cfg, rank, world, local_rank):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded Tucker/smooth tensors of BASELINE.json's configs; no dataset)",
             "config": wl, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clocks, "rhosvd_s": rhosvd_s, "rhosvd_rel_err": rel_err, "per_config": per_config,
+            "clocks": clocks, "rhosvd_s": rhosvd_s, "rhosvd_rel_err": rel_err, "rhosvd_clocks": rh_clocks,
+            "per_config": per_config,
         }
         print(json.dumps(line), flush=True)
     return 0

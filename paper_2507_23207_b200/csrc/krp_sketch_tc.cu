@@ -1268,7 +1268,7 @@ bool fill_plan(const Dims& g, int R, int m, int m2, const bool* want, bool allow
       if (fo >= 0 && oi != fo) continue;
       if (fo < 0 && (pl.R8 < o.rlo || pl.R8 > o.rhi)) continue;
       if (o.areg && ((!o.qh && pl.R8 > 48) || pl.R8 > 64)) continue;  // register accumulators: R8 <= 48 (<= 64 QH)
-      if (o.qh && o.ch == 32 && (pl.R8 < 24 || pl.R8 > 48)) continue;  // the QH instantiations
+      if (o.qh && o.ch == 32 && (pl.R8 < 24 || pl.R8 > 64 || pl.R8 == 56)) continue;  // the QH instantiations
       if (o.qh && o.ch == 16 && pl.R8 != 24 && pl.R8 != 32 && pl.R8 != 40 && pl.R8 != 56 && pl.R8 != 64) continue;
       const int dn = o.triple ? pl.N2 : (pl.R8 + R + 7) / 8 * 8;
       const int acols = o.areg ? 0 : 2 * pl.R8;
@@ -1568,6 +1568,7 @@ int tc_sketch_cols(const float* X, const Dims& g, const OmegaPtrs& om, int R, in
       case 32: kern = krp_tc_sketch_kernel<32, 32, true>; break;
       case 40: kern = krp_tc_sketch_kernel<32, 40, true>; break;
       case 48: kern = krp_tc_sketch_kernel<32, 48, true>; break;
+      case 64: kern = krp_tc_sketch_kernel<32, 64, true>; break;  // (development A/B at c5)
       default: set_error("tcgen05 sketch: no QH instantiation for CH = 32, R8 = %d", pl.RA); return KRP_EUNSUPPORTED;
     }
   } else if (pl.qh) {
