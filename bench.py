@@ -360,6 +360,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         for _ in range(min(args.warmup, 2)):
             rh()
         steps_b = max(1, min(args.steps, 10))
+        torch.cuda.synchronize()
+        time.sleep(1.0)  # power-budget recovery after phase A (its clocks are sampled and reported either way)
         tb, rh_clocks = timed(rh, steps_b, ClockSampler(gpu_index) if rank == 0 else None)
         rhosvd_s = tb / 1e3 / steps_b
         del wsr
