@@ -1011,22 +1011,33 @@ __global__ void __launch_bounds__(256, 4) tc_assemble_kernel(const __grid_consta
       const int64_t kstride = static_cast<int64_t>(kTile) * p.R;
       const uint32_t f0 = static_cast<uint32_t>(share) * F / static_cast<uint32_t>(nsplit);
       const uint32_t f1 = static_cast<uint32_t>(share + 1) * F / static_cast<uint32_t>(nsplit);
+      // (o, k) of term f, the slot-0 pointer of o's pair and its slot count, advanced incrementally
       uint32_t o = f0 / static_cast<uint32_t>(p.maxseg);
       int k = static_cast<int>(f0 - o * static_cast<uint32_t>(p.maxseg));
+      auto pair_of = [&](uint32_t oo) {
+        return rows ? blk * static_cast<uint32_t>(p.CB) + oo : oo * static_cast<uint32_t>(p.CB) + blk;
+      };
+      auto nk_of = [&](uint32_t oo) {
+        if (oo >= static_cast<uint32_t>(nother)) return 0;
+        if (spnk) return s_pnk[oo];
+        const int64_t pr = pair_of(oo);
+        return cta_of_tile((pr + 1) * p.S - 1, p.T, p.grid) - cta_of_tile(pr * p.S, p.T, p.grid) + 1;
+      };
+      const int64_t pstep = (rows ? 1 : static_cast<int64_t>(p.CB)) * p.maxseg * kstride;
+      const float* po = part + static_cast<int64_t>(pair_of(o)) * p.maxseg * kstride;
+      int nk = nk_of(o);
       for (uint32_t f = f0; f < f1; f += 16) {
         float v[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           v[i] = 0.f;
           if (f + i < f1) {
-            const uint32_t pair = rows ? blk * static_cast<uint32_t>(p.CB) + o : o * static_cast<uint32_t>(p.CB) + blk;
-            const int nk = spnk ? s_pnk[o]
-                                : cta_of_tile((static_cast<int64_t>(pair) + 1) * p.S - 1, p.T, p.grid) -
-                                      cta_of_tile(static_cast<int64_t>(pair) * p.S, p.T, p.grid) + 1;
-            if (k < nk) v[i] = __ldg(part + (static_cast<int64_t>(pair) * p.maxseg + k) * kstride);
+            if (k < nk) v[i] = __ldg(po + k * kstride);
             if (++k == p.maxseg) {
               k = 0;
               ++o;
+              po += pstep;
+              nk = nk_of(o);
             }
           }
         }
@@ -1055,12 +1066,12 @@ __global__ void __launch_bounds__(256, 4) tc_assemble_kernel(const __grid_consta
   const int64_t npairs = static_cast<int64_t>(p.RB) * p.CB;
   const int64_t p0 = w * npairs / kRedWarps, p1 = (w + 1) * npairs / kRedWarps;
   const int64_t pstride = p.S * p.R;
-  const float* src = p.Tpart + static_cast<int64_t>(idc);
+  const float* src = p.Tpart + static_cast<int64_t>(idc) + p0 * pstride;
   float acc = 0.f;
-  for (int64_t q = p0; q < p1; q += 16) {  // 16 loads in flight: a share can be hundreds of pairs long
-    float v[16];
+  for (int64_t q = p0; q < p1; q += 16, src += 16 * pstride) {  // 16 loads in flight: a share can be
+    float v[16];                                                // hundreds of pairs long
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = (q + i < p1) ? __ldg(src + (q + i) * pstride) : 0.f;
+    for (int i = 0; i < 16; ++i) v[i] = (q + i < p1) ? __ldg(src + i * pstride) : 0.f;
 #pragma unroll
     for (int i = 0; i < 16; ++i) acc += v[i];
   }
