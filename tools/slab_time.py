@@ -2,7 +2,7 @@
 
 Runs krp_sketch_all_modes_dist on rank 0's slab of an N-way split with a one-rank NCCL communicator
 (the all-reduce is then a local pass over the packed buffer), so the numbers are the per-rank compute +
-packing time of the N-GPU step without the multi-rank collective.  usage: slab_time.py <config> [steps]
+packing time of the N-GPU step without the multi-rank collective.  usage: slab_time.py <config> [steps] [worlds, e.g. 1,8]
 """
 import os
 import socket
@@ -20,6 +20,7 @@ import paper_2507_23207_b200 as krp  # noqa: E402
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "c2"
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else 50
+    worlds = [int(w) for w in sys.argv[3].split(",")] if len(sys.argv) > 3 else [1, 2, 4, 8]
     cfg = synth.config(name)
     torch.cuda.set_device(0)
     s = socket.socket()
@@ -33,7 +34,7 @@ def main():
     om = [torch.from_numpy(o).cuda() for o in synth.omegas(cfg.dims, cfg.R, 0)]
     Y = [torch.empty((n, cfg.R), dtype=torch.float32, device="cuda") for n in cfg.dims]
     base = None
-    for world in (1, 2, 4, 8):
+    for world in worlds:
         k0, kn = krp.krp_slab_range(Id, world, 0)
         dims_local = list(cfg.dims[:-1]) + [kn]
         X = torch.from_numpy(synth.tensor_slab(cfg, 0, k0, k0 + kn)).cuda()
