@@ -951,6 +951,9 @@ struct RedParams {
   int64_t M, C, S, T;
   int RB, CB, R, grid, maxseg, ldy;
   int do_p, do_q, do_t;
+  uint32_t bP, bQ;            // blocks of the P and Q regions (host-computed: no 64-bit division per block)
+  int nsP, nsQ, ncgP, ncgQ;   // term shares per column and column groups of each region
+  int unlisted;               // test hook (KRP_ASM_UNLISTED): take the long-list path at any size
   const float *partA1, *partA2, *Tpart;
   float *Pm, *Qc, *Ts;
   float *outP, *outQ, *outT;  // non-null: the group is a single wanted mode, write its Y directly
@@ -958,17 +961,20 @@ struct RedParams {
 
 // P(ρ,r) = Σ_{cb} Σ_{k < pnk[pair]} partA1[(rb*CB + cb)*maxseg + k][r][ρ%128]
 // Qc(γ,r) likewise over rb;  Ts(s,r) = Σ_{pairs} Tpart[pair][s][r].
-// P / Qc: one block = 32 consecutive rows (lanes: coalesced 128-byte partial reads) x 8/nsplit columns; the
-// F = (other blocks) x maxseg terms of a column are split into nsplit contiguous shares (one warp each, 16
-// loads in flight, (o, k) advanced incrementally), and the shares are added in order: a fixed reduction
-// order (deterministic).  nsplit grows with F so short term lists do not pay a block per column.
+// P / Qc: one block = 32 consecutive rows (lanes: coalesced 128-byte partial reads) x 8/nsplit columns.  The
+// block lists the slots its pairs used, in (o, k) order, in shared memory before the wait on the sketch
+// kernel (counts from the static tile split, a warp scan places each pair's run); each column's list is split
+// into nsplit contiguous shares (one warp each, 16 loads in flight, no per-term control flow: the per-term
+// (o, k) bookkeeping had made the kernel issue-bound, 70 % issue-active at c4), and the shares are added in
+// order: a fixed reduction order (deterministic).  nsplit grows with F = (other blocks) x maxseg so short
+// term lists do not pay a block per column; region sizes come from the host (no 64-bit division).
 // Ts: one block = 32 consecutive (s, r), the pair list split over the 8 warps (16 loads in flight), added in
-// order.  32-bit index math throughout (the plan keeps every group and table below 2^31); the slot counts
-// pnk follow from the static tile split and are formed per block before the wait on the sketch kernel.
+// order.  32-bit index math throughout (the plan keeps every group and table below 2^31).
 // A block never straddles a 128-row block (32 | 128) nor a region; a group with a single mode IS that
 // mode's sketch, so its region is written straight into Y (outP / outQ / outT non-null).
 constexpr int kRedWarps = 8;
 constexpr int kAsmMaxOther = 1024;
+constexpr int kAsmMaxTerms = 2048;  // listed term slots per block (8 KB of shared memory)
 __host__ __device__ __forceinline__ int asm_nsplit(int64_t F) {
   return F <= 32 ? 1 : (F <= 64 ? 2 : (F <= 128 ? 4 : 8));
 }
@@ -978,71 +984,91 @@ __host__ __device__ __forceinline__ int64_t asm_region_blocks(int64_t rows, int 
 }
 __global__ void __launch_bounds__(256, 4) tc_assemble_kernel(const __grid_constant__ RedParams p) {
   __shared__ float red[kRedWarps][32];
-  __shared__ int s_pnk[kAsmMaxOther];  // slots used by each pair this block reads (computed, not loaded)
+  __shared__ uint32_t s_term[kAsmMaxTerms];  // the used partial slots of this block's term list, in (o, k) order
+  __shared__ uint32_t s_cnt[kAsmMaxOther + 1];
   const int w = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
-  const int64_t FP = static_cast<int64_t>(p.CB) * p.maxseg, FQ = static_cast<int64_t>(p.RB) * p.maxseg;
-  const int64_t bP = p.do_p ? asm_region_blocks(p.M, p.R, FP) : 0, bQ = p.do_q ? asm_region_blocks(p.C, p.R, FQ) : 0;
+  const uint32_t bP = p.bP, bQ = p.bQ;
   uint32_t blk_id = blockIdx.x;
   if (blk_id < bP + bQ) {
     const bool rows = blk_id < bP;
-    if (!rows) blk_id -= static_cast<uint32_t>(bP);
+    if (!rows) blk_id -= bP;
     const int nother = rows ? p.CB : p.RB;
-    const uint32_t F = static_cast<uint32_t>(rows ? FP : FQ);
-    const int nsplit = asm_nsplit(F), cpb = kRedWarps / nsplit;
-    const uint32_t ncg = static_cast<uint32_t>((p.R + cpb - 1) / cpb);
+    const int nsplit = rows ? p.nsP : p.nsQ, cpb = kRedWarps / nsplit;
+    const uint32_t ncg = static_cast<uint32_t>(rows ? p.ncgP : p.ncgQ);
     const uint32_t rg = blk_id / ncg, cg = blk_id - rg * ncg;
     const uint32_t nrow = static_cast<uint32_t>(rows ? p.M : p.C);
     const uint32_t rho = rg * 32u + static_cast<uint32_t>(lane);
     const bool valid = rho < nrow;
     const uint32_t rc = valid ? rho : nrow - 1;
-    const uint32_t blk = rc / kTile, l = rc % kTile;
+    const uint32_t blk = rc / kTile, l = rc % kTile;  // blk is block-uniform (32 | 128)
     const int r = static_cast<int>(cg) * cpb + w / nsplit, share = w % nsplit;
-    const bool spnk = nother <= kAsmMaxOther;
-    if (spnk)
+    auto pair_of = [&](uint32_t oo) {
+      return rows ? blk * static_cast<uint32_t>(p.CB) + oo : oo * static_cast<uint32_t>(p.CB) + blk;
+    };
+    // the list of used slots (pair_of(o) * maxseg + k for k < nk(o)), formed before the wait on the sketch
+    // kernel: slot counts follow from the static tile split; a block-wide scan places each pair's run
+    const bool listed = !p.unlisted && nother <= kAsmMaxOther && static_cast<int64_t>(nother) * p.maxseg <= kAsmMaxTerms;
+    uint32_t nterm = 0;
+    if (listed) {
       for (int o = static_cast<int>(threadIdx.x); o < nother; o += blockDim.x) {
-        const int64_t pr = rows ? (static_cast<int64_t>(blk) * p.CB + o) : (static_cast<int64_t>(o) * p.CB + blk);
-        s_pnk[o] = cta_of_tile((pr + 1) * p.S - 1, p.T, p.grid) - cta_of_tile(pr * p.S, p.T, p.grid) + 1;
+        const int64_t pr = pair_of(static_cast<uint32_t>(o));
+        s_cnt[o + 1] = static_cast<uint32_t>(cta_of_tile((pr + 1) * p.S - 1, p.T, p.grid) -
+                                             cta_of_tile(pr * p.S, p.T, p.grid) + 1);
       }
-    __syncthreads();
+      __syncthreads();
+      if (w == 0) {  // inclusive scan of s_cnt[1..nother] by warp 0 (32 entries per round)
+        uint32_t carry = 0;
+        for (int o0 = 0; o0 < nother; o0 += 32) {
+          const int o = o0 + lane;
+          uint32_t v = o < nother ? s_cnt[o + 1] : 0u;
+#pragma unroll
+          for (int m = 1; m < 32; m <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, v, m);
+            if (lane >= m) v += u;
+          }
+          if (o < nother) s_cnt[o + 1] = carry + v;
+          carry += __shfl_sync(0xffffffffu, v, 31);
+        }
+        if (lane == 0) s_cnt[0] = 0;
+      }
+      __syncthreads();
+      for (int o = static_cast<int>(threadIdx.x); o < nother; o += blockDim.x) {
+        const uint32_t b0 = s_cnt[o], n = s_cnt[o + 1] - b0;
+        const uint32_t slot0 = pair_of(static_cast<uint32_t>(o)) * static_cast<uint32_t>(p.maxseg);
+        for (uint32_t k = 0; k < n; ++k) s_term[b0 + k] = slot0 + k;
+      }
+      __syncthreads();
+      nterm = s_cnt[nother];
+    }
     pdl_wait();  // the partials are written by the sketch kernel
     float acc = 0.f;
     if (r < p.R) {
       const float* part = (rows ? p.partA1 : p.partA2) + static_cast<int64_t>(r) * kTile + l;
       const int64_t kstride = static_cast<int64_t>(kTile) * p.R;
-      const uint32_t f0 = static_cast<uint32_t>(share) * F / static_cast<uint32_t>(nsplit);
-      const uint32_t f1 = static_cast<uint32_t>(share + 1) * F / static_cast<uint32_t>(nsplit);
-      // (o, k) of term f, the slot-0 pointer of o's pair and its slot count, advanced incrementally
-      uint32_t o = f0 / static_cast<uint32_t>(p.maxseg);
-      int k = static_cast<int>(f0 - o * static_cast<uint32_t>(p.maxseg));
-      auto pair_of = [&](uint32_t oo) {
-        return rows ? blk * static_cast<uint32_t>(p.CB) + oo : oo * static_cast<uint32_t>(p.CB) + blk;
-      };
-      auto nk_of = [&](uint32_t oo) {
-        if (oo >= static_cast<uint32_t>(nother)) return 0;
-        if (spnk) return s_pnk[oo];
-        const int64_t pr = pair_of(oo);
-        return cta_of_tile((pr + 1) * p.S - 1, p.T, p.grid) - cta_of_tile(pr * p.S, p.T, p.grid) + 1;
-      };
-      const int64_t pstep = (rows ? 1 : static_cast<int64_t>(p.CB)) * p.maxseg * kstride;
-      const float* po = part + static_cast<int64_t>(pair_of(o)) * p.maxseg * kstride;
-      int nk = nk_of(o);
-      for (uint32_t f = f0; f < f1; f += 16) {
-        float v[16];
+      if (listed) {
+        // share `share` of the used terms, 16 loads in flight, no per-term control flow
+        const uint32_t f0 = static_cast<uint32_t>(share) * nterm / static_cast<uint32_t>(nsplit);
+        const uint32_t f1 = static_cast<uint32_t>(share + 1) * nterm / static_cast<uint32_t>(nsplit);
+        for (uint32_t f = f0; f < f1; f += 16) {
+          float v[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          v[i] = 0.f;
-          if (f + i < f1) {
-            if (k < nk) v[i] = __ldg(po + k * kstride);
-            if (++k == p.maxseg) {
-              k = 0;
-              ++o;
-              po += pstep;
-              nk = nk_of(o);
-            }
-          }
+          for (int i = 0; i < 16; ++i)
+            v[i] = f + i < f1 ? __ldg(part + static_cast<int64_t>(s_term[f + i]) * kstride) : 0.f;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc += v[i];
         }
-#pragma unroll
-        for (int i = 0; i < 16; ++i) acc += v[i];  // unused slots add an exact 0
+      } else {
+        // long term lists: walk every (o, k) slot, unused slots add an exact 0
+        const uint32_t F = static_cast<uint32_t>(nother) * static_cast<uint32_t>(p.maxseg);
+        const uint32_t f0 = static_cast<uint32_t>(share) * F / static_cast<uint32_t>(nsplit);
+        const uint32_t f1 = static_cast<uint32_t>(share + 1) * F / static_cast<uint32_t>(nsplit);
+        for (uint32_t f = f0; f < f1; ++f) {
+          const uint32_t o = f / static_cast<uint32_t>(p.maxseg);
+          const int k = static_cast<int>(f - o * static_cast<uint32_t>(p.maxseg));
+          const int64_t pr = pair_of(o);
+          const int nk = cta_of_tile((pr + 1) * p.S - 1, p.T, p.grid) - cta_of_tile(pr * p.S, p.T, p.grid) + 1;
+          if (k < nk) acc += __ldg(part + (pr * p.maxseg + k) * kstride);
+        }
       }
     }
     red[w][lane] = acc;
@@ -1056,7 +1082,7 @@ __global__ void __launch_bounds__(256, 4) tc_assemble_kernel(const __grid_consta
     }
     return;
   }
-  blk_id -= static_cast<uint32_t>(bP + bQ);
+  blk_id -= bP + bQ;
   const uint32_t nT = static_cast<uint32_t>(p.S) * static_cast<uint32_t>(p.R);
   const uint32_t idx = blk_id * 32u + static_cast<uint32_t>(lane);
   pdl_wait();  // Tpart is written by the sketch kernel
@@ -1654,6 +1680,17 @@ int tc_sketch_cols(const float* X, const Dims& g, const OmegaPtrs& om, int R, in
       // multi-TTV reads them in place and the assembly skips the slice region
       Ts = p.Tpart;
       rp.do_t = 0;
+    }
+    {
+      const int64_t FP = static_cast<int64_t>(pl.CB) * pl.maxseg, FQ = static_cast<int64_t>(pl.RB) * pl.maxseg;
+      rp.nsP = asm_nsplit(FP);
+      rp.nsQ = asm_nsplit(FQ);
+      rp.ncgP = (R + kRedWarps / rp.nsP - 1) / (kRedWarps / rp.nsP);
+      rp.ncgQ = (R + kRedWarps / rp.nsQ - 1) / (kRedWarps / rp.nsQ);
+      rp.bP = static_cast<uint32_t>(rp.do_p ? asm_region_blocks(pl.M, R, FP) : 0);
+      rp.bQ = static_cast<uint32_t>(rp.do_q ? asm_region_blocks(pl.C, R, FQ) : 0);
+      const char* ul = getenv("KRP_ASM_UNLISTED");
+      rp.unlisted = ul && ul[0] == '1';
     }
     const int64_t nblk = assemble_blocks(pl.M, pl.C, pl.S, R, rp.do_p, rp.do_q, rp.do_t, pl.RB, pl.CB, pl.maxseg);
     KRP_CHECK_CUDA(launch_pdl(tc_assemble_kernel, dim3(static_cast<unsigned>(nblk)), dim3(256), 0, s, rp));

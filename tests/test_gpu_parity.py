@@ -182,6 +182,22 @@ def test_sketch_is_deterministic(krp):
         assert torch.equal(u, v)
 
 
+@pytest.mark.parametrize("dims,R", [((256, 256, 64), 40), ((64, 32, 16, 8, 6), 20)])
+def test_assembly_long_list_path(krp, dims, R, monkeypatch):
+    """The assembly's two term-list paths (listed used slots / every (pair, slot) walked) give the same
+    sums up to summation grouping (P(rho, r) = sum over col blocks and CTA slots)."""
+    x = _dev(synth.random_tensor(dims, 13))
+    om = [_dev(o) for o in synth.omegas(dims, R, 13)]
+    a = krp.krp_sketch_all_modes(x, dims, om)
+    monkeypatch.setenv("KRP_ASM_UNLISTED", "1")
+    b = krp.krp_sketch_all_modes(x, dims, om)
+    ref = oracle.sketch_all_modes(oracle.as_tensor(x.cpu().numpy(), dims), [o.cpu().numpy() for o in om])
+    for n, (u, v) in enumerate(zip(a, b)):
+        scale = float(np.abs(ref[n]).max())
+        assert float((u - v).abs().max()) <= 1e-6 * scale, n
+        assert float((v.double().cpu() - torch.from_numpy(ref[n])).abs().max()) <= 1e-5 * scale, n
+
+
 # ----------------------------------------------------------------- the core contraction (mode-n product)
 # Mode 0 with I_1 % 4 == 0 and J <= 64 runs on the tcgen05 3xTF32 kernel; the shapes below span several
 # 128-column tiles with a ragged last tile, K chunks with a ragged tail (I_1 = 36, 100), J = 1 .. 64 and
