@@ -135,16 +135,24 @@ def _cores():
 
 
 def _calibrate_slabs(cfg, seed, om, target_s):
-    """Number of last-mode slabs whose oracle sketch takes about target_s (doubling calibration)."""
-    slabs, t = 1, 0.0
-    while slabs < cfg.dims[-1]:
-        t, _ = _oracle_sample(cfg, seed, slabs, om)
-        if t >= 0.25 * target_s:
+    """Number of last-mode slabs whose oracle sketch takes about target_s.  The oracle's time is affine in
+    the slab count (forming the explicit Khatri-Rao matrix of the last mode's sketch costs the same for any
+    slab), so two samples fit t = a + b * slabs; a proportional fit would stop at a sample that is almost all
+    fixed cost (c5: 3 of 512 slabs)."""
+    Id = cfg.dims[-1]
+    s1, t1 = 1, 0.0
+    while s1 < Id:
+        t1, _ = _oracle_sample(cfg, seed, s1, om)
+        if t1 >= 0.25 * target_s:
             break
-        slabs = min(cfg.dims[-1], slabs * 2)
-    if t > 0:
-        slabs = int(max(1, min(cfg.dims[-1], slabs * target_s / t)))
-    return slabs
+        s1 = min(Id, s1 * 2)
+    if s1 >= Id or t1 <= 0 or t1 >= target_s:
+        return int(max(1, min(Id, s1 * target_s / t1))) if t1 > 0 else s1
+    s2 = min(Id, max(s1 + 1, 4 * s1))
+    t2, _ = _oracle_sample(cfg, seed, s2, om)
+    b = max((t2 - t1) / (s2 - s1), 0.01 * t1 / s1)  # floor: a noisy pair must not extrapolate without bound
+    a = max(t1 - b * s1, 0.0)
+    return int(max(1, min(Id, (target_s - a) / b)))
 
 
 def cpu_baseline(cfg, seed, om, target_s=12.0):
