@@ -1,9 +1,6 @@
-T=gpurun_out/tg4
-mkdir -p $T
-{
-for c in c4 c3 c2 c4 c3 c2; do
-  echo "== head"; KRP_LIB=abtest/libkrp_head.so timeout 120 python tools/rh_time.py $c 5
-  echo "== new";  timeout 120 python tools/rh_time.py $c 5
-done
-} > $T/log 2>&1
-timeout 1500 python -m pytest tests -m gpu -x -q > $T/pytest.log 2>&1
+#!/bin/bash
+# re-run of the default bench (both arms) after the oracle-sample calibration change
+OUT=gpurun_out/r02m; mkdir -p $OUT
+( time timeout 900 python bench.py ) > $OUT/bench_c5.log 2>&1; echo "rc=$?" >> $OUT/bench_c5.log
+( time timeout 900 python bench.py --impl reference ) > $OUT/bench_reference_default.log 2>&1; echo "rc=$?" >> $OUT/bench_reference_default.log
+( time timeout 900 python bench.py --config c4 --no-per-config ) > $OUT/bench_c4.log 2>&1; echo "rc=$?" >> $OUT/bench_c4.log
