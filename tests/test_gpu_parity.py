@@ -101,6 +101,8 @@ SHAPES = [
     # degenerate cases: R = 1, unit modes (first, middle, last), a single-element tensor, d = 2
     ((128, 128, 128), 1), ((1, 128, 256), 8), ((128, 1, 256), 8), ((256, 128, 1), 8), ((1, 1, 1), 1),
     ((300, 260), 33), ((1, 7), 1),
+    # the largest order the boundary accepts (d = 8, krp.h) and d = 7
+    ((4, 3, 2, 3, 2, 2, 3), 5), ((3, 2, 4, 2, 3, 2, 2, 5), 6), ((130, 2, 2, 2, 2, 2, 2, 2), 9),
 ]
 
 
@@ -335,6 +337,29 @@ def test_sthosvd_parity(krp, small):
     _check_factors(Q, cfg.ranks)
     assert abs(err - err_ref) <= ERR_TOL, (err, err_ref)
     _sthosvd_step_checks(krp, x, cfg.dims, oms, cfg.ranks, Q)
+
+
+def test_rhosvd_and_sthosvd_at_the_maximum_order(krp):
+    """d = 8, the largest order the boundary accepts (krp.h): rHOSVD (Alg. 7) and STHOSVD (Alg. 8) errors
+    match the oracle on a small noisy Tucker tensor with truncation (r < R)."""
+    cfg = synth.Config("d8", (6, 5, 4, 4, 3, 3, 3, 4), 3, (2,) * 8, "tucker", core=(2,) * 8, eta=1e-3)
+    x = synth.tensor(cfg, 3)
+    X = oracle.as_tensor(x, cfg.dims)
+    om = synth.omegas(cfg.dims, cfg.R, 3)
+    _, _, err_ref, _ = oracle.rhosvd(X, om, cfg.ranks)
+    Q, core, err = krp.krp_rhosvd(_dev(x), cfg.dims, cfg.ranks, [_dev(o) for o in om], with_error=True)
+    _check_factors(Q, cfg.ranks)
+    assert core.numel() == 2 ** 8
+    assert abs(err - err_ref) <= ERR_TOL, (err, err_ref)
+    g = core.double().cpu().numpy().reshape(cfg.ranks, order="F")
+    e2 = oracle.tucker_error(X, g, [q.double().cpu().numpy() for q in Q])
+    assert abs(e2 - err) <= 1e-5 + 1e-3 * err
+    oms = synth.sthosvd_omegas(cfg.dims, cfg.R, 3)
+    _, _, serr_ref, _ = oracle.sthosvd(X, oms, cfg.ranks)
+    dom = [[None if o is None else _dev(o) for o in row] for row in oms]
+    Qs, _, serr = krp.krp_sthosvd(_dev(x), cfg.dims, cfg.ranks, dom, with_error=True)
+    _check_factors(Qs, cfg.ranks)
+    assert abs(serr - serr_ref) <= ERR_TOL, (serr, serr_ref)
 
 
 # ----------------------------------------------------------------- NEXT-1: the paper's Cauchy workload
