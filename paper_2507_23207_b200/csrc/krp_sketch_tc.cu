@@ -174,6 +174,12 @@ __host__ __device__ __forceinline__ int cta_of_tile(int64_t t, int64_t T, int gr
 #ifndef KRP_SKETCH_PDL
 #define KRP_SKETCH_PDL 0
 #endif
+// L2 prefetch distance of the TMA producer, in tiles; -1 = per plan (profiles/r02o_ab_prefetch_distance.log:
+// with >= 2 shared-memory stages the TMA loads themselves run far enough ahead and the extra prefetch requests
+// cost 2 % at c2-c4; with c5's single stage one tile ahead pays, deeper distances lose everywhere)
+#ifndef KRP_PF
+#define KRP_PF -1
+#endif
 #ifndef KRP_SPLIT_BATCH
 #define KRP_SPLIT_BATCH 1
 #endif
@@ -399,8 +405,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t ph = 0;
       int64_t pair = t0 / p.S, s = t0 % p.S;
       int rb = static_cast<int>(pair / p.CB), cb = static_cast<int>(pair % p.CB);
-      // L2 prefetch runs kPf tiles ahead of the loads (hides DRAM hiccups behind only NS SMEM stages)
-      constexpr int kPf = 3;
+      // L2 prefetch runs kPf tiles ahead of the loads: only where a single SMEM stage leaves the loads no lead
+      const int kPf = KRP_PF >= 0 ? KRP_PF : (p.NS >= 2 ? 0 : 1);
       int64_t pf_t = t0, pf_pair = pair, pf_s = s;
       auto pf_issue = [&]() {
         const int pp = static_cast<int>(pf_pair), prb = pp / p.CB, pcb = pp - prb * p.CB;  // 32-bit division
@@ -413,7 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       for (int i = 0; i < kPf && pf_t < t1; ++i) pf_issue();
       for (int64_t t = t0; t < t1; ++t) {
-        if (pf_t < t1) pf_issue();
+        if (kPf > 0 && pf_t < t1) pf_issue();
         KWAIT(&empty_x[st], ph ^ 1);
         KRP_TRACE(0, t - t0);
         if (KRP_DBG(1)) {  // probe: no data movement (the stage holds whatever it held)
